@@ -1,0 +1,164 @@
+/*
+ * dawn.h — C ABI of the B200-native weighted-DAWN shortest-path library (libdawn.so).
+ *
+ * This is the drop-in boundary for the reference package `sparsepath`
+ * (/root/reference/pkg/src/sparsepath).  Every entry point below replaces one
+ * function of the reference's hot path; the citation next to each one names
+ * the reference symbol (file:line) whose behaviour it reproduces.  The
+ * reference is pure Python, so the "FFI binding a maintainer would add" is a
+ * ctypes stub; INTEGRATION.md shows it.
+ *
+ * Conventions
+ *   - All functions return an int status: DAWN_OK (0) or a DAWN_E* code.
+ *     dawn_last_error() returns a thread-local message for the last failure.
+ *   - Plain pointers and sizes only.  `stream` is a cudaStream_t passed as
+ *     void* (NULL = legacy default stream).
+ *   - Host arrays use the reference's CsrGraph layout (graph.py:64-109):
+ *     int64 row_ptr[n+1], int64 col[m], float64 val[m].
+ *   - Distances come back as float64 with +inf for unreachable nodes, the
+ *     reference's DistanceVector.dist contract (solver.py:66-71).
+ *   - Negative cycles are not errors: they set dawn_stats_t.negative_cycle,
+ *     as the reference does (solver.py:17-24).
+ *   - No CPU fallback: every solve runs on the GPU; without a CUDA device the
+ *     calls fail with DAWN_ECUDA.
+ */
+#ifndef DAWN_H_
+#define DAWN_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DAWN_ABI_VERSION 1
+
+/* status codes */
+#define DAWN_OK 0
+#define DAWN_EINVAL 1        /* bad argument (maps to ValueError) */
+#define DAWN_ESOURCE 2       /* source out of range (ValueError "source s out of range for n=N", solver.py:253-255) */
+#define DAWN_ECUDA 3         /* CUDA runtime failure / no device (RuntimeError) */
+#define DAWN_ENOMEM 4        /* device allocation failed */
+#define DAWN_EUNSUPPORTED 5  /* graph too large for the packed frontier reservation, etc. */
+
+/* value (distance/weight) types on the device */
+#define DAWN_I32 0
+#define DAWN_I64 1
+#define DAWN_F32 2
+#define DAWN_F64 3
+
+/* precision policy for dawn_choose_vtype */
+#define DAWN_PREC_AUTO 0  /* integral weights -> I32/I64 (bit-exact vs the fp64 reference); else F64 */
+#define DAWN_PREC_FP32 1  /* opt-in: F32 weights and accumulation (<= 1e-6 relative, north_star) */
+#define DAWN_PREC_FP64 2  /* always F64 (bit-exact vs the reference's Python floats) */
+
+/* algorithms (the reference's SOLVERS registry, solver.py:402) */
+#define DAWN_GOVM 0  /* frontier rescans, govm_sssp solver.py:324-399 */
+#define DAWN_GSVM 1  /* full rescans,     gsvm_sssp solver.py:265-321 */
+
+/* solve flags */
+#define DAWN_F_PRED 1u        /* record predecessors (record_pred=True, solver.py:309-310, :383-384) */
+#define DAWN_F_NEGCHECK 2u    /* early negative-cycle exit via predecessor-graph cycle check
+                                 (integer types only; same verdict as the n-round cap, solver.py:394-395) */
+
+typedef struct dawn_graph_s* dawn_graph_t;
+typedef struct dawn_solver_s* dawn_solver_t;
+
+/* Per-solve counters (SolveStats, solver.py:118-149).  Counts follow
+ * snapshot-Jacobi round semantics (SURVEY §8(a) conventions 1-7):
+ * `writes` counts (node, round) changes, `multi_written` the nodes changed in
+ * >= 2 rounds (numerator of updated_ratio, solver.py:258-262). */
+typedef struct {
+  int64_t outer_steps;
+  int64_t relaxations;
+  int64_t writes;
+  int64_t first_discoveries;
+  int64_t multi_written;
+  int32_t negative_cycle;
+  int32_t early_exit;   /* 1 when DAWN_F_NEGCHECK stopped the solve before the cap */
+} dawn_stats_t;
+
+int dawn_abi_version(void);
+const char* dawn_last_error(void);
+int dawn_device_count(int* count_out);
+
+/* Precision probe: picks the device value type for a float64 weight array
+ * (CsrGraph.val, graph.py:85-87).  AUTO chooses I32 when every weight is
+ * integral and n*max|w| fits in int32, I64 when it fits in 2^53 (where the
+ * reference's float64 sums are still exact), else F64. */
+int dawn_choose_vtype(int64_t n, int64_t m, const double* val, int precision, int* vtype_out);
+
+/* Upload an immutable CSR graph (CsrGraph, graph.py:64-109) to `device`.
+ * row_ptr/col/val are host pointers unless src_is_device != 0, in which case
+ * they are device pointers on `device`.  Weights are converted to `vtype`;
+ * for integer vtypes a non-integral or out-of-range weight is DAWN_EINVAL
+ * (never silently truncated, SURVEY §8(b) constraint 5). */
+int dawn_graph_create(int device, int64_t n, int64_t m, const int64_t* row_ptr,
+                      const int64_t* col, const double* val, int vtype, int src_is_device,
+                      dawn_graph_t* out);
+int dawn_graph_destroy(dawn_graph_t g);
+int dawn_graph_info(dawn_graph_t g, int64_t* n, int64_t* m, int* vtype, int64_t* device_bytes);
+
+/* A solver owns the per-solve device workspace for one graph (dist keys,
+ * write stamps, two frontier queues, tile map).  One solver per concurrent
+ * stream; the graph itself is shareable.  flags: DAWN_F_PRED reserves the
+ * predecessor arrays. */
+int dawn_solver_create(dawn_graph_t g, unsigned flags, dawn_solver_t* out);
+int dawn_solver_destroy(dawn_solver_t s);
+
+/* One single-source solve: govm_sssp / gsvm_sssp (solver.py:265-399),
+ * including the seeding round seed_source (solver.py:212-250).
+ *   dist_out  : float64[n], host or device pointer, or NULL to keep the
+ *               result device-resident (read later with dawn_solver_result).
+ *   pred_out  : int64[n] (-1 = None), host or device, or NULL.  Requires
+ *               DAWN_F_PRED in `flags` and in the solver's flags.
+ *   stats_out : if non-NULL the call synchronises `stream` and fills it;
+ *               if NULL the call is fully asynchronous.
+ * Source range is checked before any device work (DAWN_ESOURCE). */
+int dawn_sssp(dawn_solver_t s, int64_t source, int algo, unsigned flags, double* dist_out,
+              int64_t* pred_out, dawn_stats_t* stats_out, void* stream);
+
+/* Debug stepping for the reference's `trace` hook (solver.py:328-336,
+ * :386-387): begin a solve, then advance at most `max_rounds` rounds per call
+ * (each call synchronises).  round_out receives the last completed round
+ * (step), done_out 1 once the solve has terminated. */
+int dawn_sssp_begin(dawn_solver_t s, int64_t source, int algo, unsigned flags, void* stream);
+int dawn_sssp_advance(dawn_solver_t s, int max_rounds, int64_t* round_out, int* done_out,
+                      void* stream);
+/* Asynchronous advance (no synchronisation, no state read-back): runs at
+ * most `max_rounds` rounds (0 = to completion) of the solve begun with
+ * dawn_sssp_begin.  Used to time the persistent kernel alone. */
+int dawn_sssp_run(dawn_solver_t s, int max_rounds, void* stream);
+/* Copy out the current state: dist (float64[n]) and the per-node write stamp
+ * (uint32[n]: stamp>>1 = last round that lowered the node, bit0 = lowered in
+ * >= 2 rounds).  Any pointer may be NULL.  Synchronises `stream`. */
+int dawn_solver_state(dawn_solver_t s, double* dist_out, uint32_t* stamp_out, void* stream);
+/* Result of the last solve on this solver (after dawn_sssp with NULL
+ * outputs, or after stepping finished). Synchronises `stream`. */
+int dawn_solver_result(dawn_solver_t s, double* dist_out, int64_t* pred_out,
+                       dawn_stats_t* stats_out, void* stream);
+
+/* Multi-source: independent solves from sources[0..k) (host int64 array) in
+ * the given order — mssp (solver.py:426-457).  dist_out is a row-major
+ * float64 [k][n] tile (host or device) or NULL; stats_out a host array of k
+ * entries or NULL.  All sources are validated before any work
+ * (solver.py:441-443).  One synchronisation at the end. */
+int dawn_mssp(dawn_solver_t s, const int64_t* sources, int64_t k, int algo, unsigned flags,
+              double* dist_out, dawn_stats_t* stats_out, void* stream);
+
+/* Synthetic generators on the device (SURVEY §8(f) row F1 inputs).  They
+ * write an edge list (u, v, w) of m edges, deterministic in `seed` through a
+ * counter-based hash, identical to the host restatement in
+ * paper_2306_07872_b200/generators.py.
+ *   rmat : Graph500 quadrant probabilities a,b,c (d = 1-a-b-c), 2^scale nodes,
+ *          m = edge_factor * 2^scale edges; duplicates and self-loops kept.
+ *   wkind: 0 = integer uniform in [wlo, whi] ; 1 = float32 uniform in [0,1). */
+int dawn_gen_rmat(int device, int scale, int64_t edge_factor, double a, double b, double c,
+                  uint64_t seed, int wkind, int64_t wlo, int64_t whi, uint64_t wseed,
+                  int64_t* u_out, int64_t* v_out, double* w_out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DAWN_H_ */

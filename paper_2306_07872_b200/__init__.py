@@ -1,0 +1,65 @@
+"""B200-native weighted DAWN (arXiv 2306.07872): GOVM/GSVM shortest paths.
+
+Drop-in for the hot path of the reference package ``sparsepath``: the same
+solver names, signatures, return types and error behaviour, executed by
+hand-written sm_100a CUDA kernels behind the C ABI in ``include/dawn.h``
+(``libdawn.so``, loaded through ctypes).  There is no CPU fallback.
+"""
+
+from .device import DeviceGraph, clear_cache, device_graph, get_default_precision, set_default_precision
+from .graph import (
+    CsrGraph,
+    EdgeList,
+    WeightMode,
+    apply_weight_mode,
+    build_csr,
+    csr_from_arrays,
+    generate_random_graph,
+    to_edge_list,
+)
+from .solver import (
+    SOLVERS,
+    AggregateStats,
+    DistanceVector,
+    FrontierFlags,
+    PredecessorVector,
+    SolveStats,
+    aggregate_stats,
+    apsp,
+    format_distance_row,
+    govm_sssp,
+    gsvm_sssp,
+    mssp,
+    seed_source,
+)
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "CsrGraph",
+    "EdgeList",
+    "WeightMode",
+    "apply_weight_mode",
+    "build_csr",
+    "csr_from_arrays",
+    "generate_random_graph",
+    "to_edge_list",
+    "DistanceVector",
+    "PredecessorVector",
+    "FrontierFlags",
+    "SolveStats",
+    "AggregateStats",
+    "seed_source",
+    "gsvm_sssp",
+    "govm_sssp",
+    "mssp",
+    "apsp",
+    "aggregate_stats",
+    "format_distance_row",
+    "SOLVERS",
+    "DeviceGraph",
+    "device_graph",
+    "clear_cache",
+    "set_default_precision",
+    "get_default_precision",
+]

@@ -1,0 +1,729 @@
+// dawn.cu — C ABI (include/dawn.h) over the sm_100a weighted-DAWN kernels.
+//
+// Memory model: the graph and each solver's workspace are allocated once
+// (cudaMalloc, outside any solve); a solve performs no allocation.  Device
+// layout per graph (32-bit indices when m < 2^32):
+//   row_ptr : EI[n+1]
+//   edges   : uint2 {col, weight bits}[m]        (4-byte value types: 8 B/edge, one LDG.64)
+//             uint32 col[m] + uint64 w[m]         (8-byte value types: 12 B/edge)
+// Per solver: dist keys K[n], write stamps u32[n], two frontier queues
+// {node u32, off EI, base EI, key K}[n], a tile->row map u32[m/TILE+2], and
+// the DevState block.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <type_traits>
+#include <climits>
+#include <string>
+
+#include "../../include/dawn.h"
+#include "dawn_kernels.cuh"
+
+using namespace dawn;
+
+// ---------------------------------------------------------------------------
+// errors
+// ---------------------------------------------------------------------------
+static thread_local std::string g_last_error;
+
+static int fail(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+#define CK(expr)                                                                          \
+  do {                                                                                    \
+    cudaError_t e_ = (expr);                                                              \
+    if (e_ != cudaSuccess) {                                                              \
+      return fail(e_ == cudaErrorMemoryAllocation ? DAWN_ENOMEM : DAWN_ECUDA, "%s: %s (%s:%d)", \
+                  #expr, cudaGetErrorString(e_), __FILE__, __LINE__);                     \
+    }                                                                                     \
+  } while (0)
+
+#define TRY(expr)              \
+  do {                         \
+    int rc_ = (expr);          \
+    if (rc_ != DAWN_OK) return rc_; \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// objects
+// ---------------------------------------------------------------------------
+struct dawn_graph_s {
+  int device = 0;
+  int64_t n = 0, m = 0;
+  int vtype = DAWN_F64;
+  bool wide = false;      // 64-bit edge indices
+  bool has_negative = false;
+  void* row_ptr = nullptr;
+  uint2* e2 = nullptr;
+  uint32_t* ecol = nullptr;
+  unsigned long long* ew = nullptr;
+  int64_t bytes = 0;
+};
+
+struct dawn_solver_s {
+  dawn_graph_t g = nullptr;
+  unsigned flags = 0;
+  void* dist = nullptr;
+  uint32_t* stamp = nullptr;
+  unsigned long long* pred = nullptr;
+  uint32_t* jmp0 = nullptr;
+  uint32_t* jmp1 = nullptr;
+  uint32_t* qnode[2] = {nullptr, nullptr};
+  void* qoff[2] = {nullptr, nullptr};
+  void* qbase[2] = {nullptr, nullptr};
+  void* qkey[2] = {nullptr, nullptr};
+  uint32_t* tile_row = nullptr;
+  DevState* st = nullptr;
+  DevState* st_host = nullptr;  // pinned
+  double* dbuf = nullptr;
+  int64_t* pbuf = nullptr;
+  int grid = 1;
+  size_t smem = 0;
+  int ebits = 32;
+  int logn = 0;
+  // current solve
+  int64_t source = -1;
+  int algo = 0;
+  unsigned run_flags = 0;
+  bool active = false;
+};
+
+static int bitlen(uint64_t x) {
+  int b = 0;
+  while (x) { ++b; x >>= 1; }
+  return b;
+}
+
+static bool is_device_ptr(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// ---------------------------------------------------------------------------
+// graph upload / conversion kernels
+// ---------------------------------------------------------------------------
+enum : unsigned { ERR_COL = 1u, ERR_NONINT = 2u, ERR_RANGE = 4u, NEG = 8u, ERR_ROWPTR = 16u };
+
+template <class V>
+__global__ void k_convert_edges(const int64_t* __restrict__ col, const double* __restrict__ val,
+                                int64_t m, int64_t n, uint2* __restrict__ e2,
+                                uint32_t* __restrict__ ecol, unsigned long long* __restrict__ ew,
+                                unsigned* flags) {
+  unsigned f = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = col[i];
+    if (c < 0 || c >= n) f |= ERR_COL;
+    const double w = val[i];
+    if (w < 0) f |= NEG;
+    if constexpr (sizeof(V) == 4) {
+      uint32_t wb;
+      if constexpr (std::is_same<V, int32_t>::value) {
+        if (w != rint(w)) f |= ERR_NONINT;
+        if (!(fabs(w) <= 2147483647.0)) f |= ERR_RANGE;
+        wb = (uint32_t)(int32_t)w;
+      } else {
+        float x = (float)w;
+        if (isinf(x)) f |= ERR_RANGE;
+        wb = __float_as_uint(x);
+      }
+      e2[i] = make_uint2((uint32_t)c, wb);
+    } else {
+      unsigned long long wb;
+      if constexpr (std::is_same<V, int64_t>::value) {
+        if (w != rint(w)) f |= ERR_NONINT;
+        if (!(fabs(w) < 9223372036854775807.0)) f |= ERR_RANGE;
+        wb = (unsigned long long)(long long)w;
+      } else {
+        wb = (unsigned long long)__double_as_longlong(w);
+      }
+      ecol[i] = (uint32_t)c;
+      ew[i] = wb;
+    }
+  }
+  if (f) atomicOr(flags, f);
+}
+
+template <class EI>
+__global__ void k_convert_rowptr(const int64_t* __restrict__ rp, int64_t n, int64_t m,
+                                 EI* __restrict__ out, unsigned* flags) {
+  unsigned f = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t a = rp[i];
+    if (i == 0 && a != 0) f |= ERR_ROWPTR;
+    if (i == n && a != m) f |= ERR_ROWPTR;
+    if (i < n && rp[i + 1] < a) f |= ERR_ROWPTR;
+    out[i] = (EI)a;
+  }
+  if (f) atomicOr(flags, f);
+}
+
+static int value_size(int vtype) { return (vtype == DAWN_I32 || vtype == DAWN_F32) ? 4 : 8; }
+
+extern "C" int dawn_abi_version(void) { return DAWN_ABI_VERSION; }
+extern "C" const char* dawn_last_error(void) { return g_last_error.c_str(); }
+
+extern "C" int dawn_device_count(int* count_out) {
+  if (!count_out) return fail(DAWN_EINVAL, "count_out is NULL");
+  int c = 0;
+  cudaError_t e = cudaGetDeviceCount(&c);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    *count_out = 0;
+    return fail(DAWN_ECUDA, "cudaGetDeviceCount: %s", cudaGetErrorString(e));
+  }
+  *count_out = c;
+  return DAWN_OK;
+}
+
+extern "C" int dawn_choose_vtype(int64_t n, int64_t m, const double* val, int precision,
+                                 int* vtype_out) {
+  if (!vtype_out || n < 0 || m < 0 || (m > 0 && !val)) return fail(DAWN_EINVAL, "bad arguments");
+  if (precision == DAWN_PREC_FP32) { *vtype_out = DAWN_F32; return DAWN_OK; }
+  if (precision == DAWN_PREC_FP64) { *vtype_out = DAWN_F64; return DAWN_OK; }
+  if (precision != DAWN_PREC_AUTO) return fail(DAWN_EINVAL, "unknown precision %d", precision);
+  bool integral = true;
+  double maxabs = 0.0;
+  for (int64_t i = 0; i < m; ++i) {
+    const double w = val[i];
+    if (!isfinite(w)) return fail(DAWN_EINVAL, "weights must be finite");
+    if (integral && w != floor(w)) integral = false;
+    maxabs = std::max(maxabs, fabs(w));
+  }
+  if (!integral) { *vtype_out = DAWN_F64; return DAWN_OK; }
+  // |dist| after r rounds is at most r*max|w| with r <= n; one more edge for the candidate.
+  const double bound = ((double)n + 1.0) * maxabs;
+  if (bound < 2147483647.0) *vtype_out = DAWN_I32;
+  else if (bound < 9007199254740992.0) *vtype_out = DAWN_I64;  // 2^53: reference fp64 sums exact
+  else *vtype_out = DAWN_F64;
+  return DAWN_OK;
+}
+
+template <class V>
+static int convert_graph(dawn_graph_t g, const int64_t* d_rp, const int64_t* d_col,
+                         const double* d_val, unsigned* d_flags) {
+  const int64_t n = g->n, m = g->m;
+  const int blocks = 148 * 8;
+  if (g->wide) {
+    k_convert_rowptr<unsigned long long><<<blocks, 256>>>(d_rp, n, m, (unsigned long long*)g->row_ptr, d_flags);
+  } else {
+    k_convert_rowptr<uint32_t><<<blocks, 256>>>(d_rp, n, m, (uint32_t*)g->row_ptr, d_flags);
+  }
+  CK(cudaGetLastError());
+  if (m > 0) {
+    k_convert_edges<V><<<blocks, 256>>>(d_col, d_val, m, n, g->e2, g->ecol, g->ew, d_flags);
+    CK(cudaGetLastError());
+  }
+  return DAWN_OK;
+}
+
+static void graph_free(dawn_graph_t g) {
+  if (!g) return;
+  cudaSetDevice(g->device);
+  cudaFree(g->row_ptr);
+  cudaFree(g->e2);
+  cudaFree(g->ecol);
+  cudaFree(g->ew);
+  delete g;
+}
+
+extern "C" int dawn_graph_create(int device, int64_t n, int64_t m, const int64_t* row_ptr,
+                                 const int64_t* col, const double* val, int vtype,
+                                 int src_is_device, dawn_graph_t* out) {
+  if (!out) return fail(DAWN_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (n < 1 || m < 0 || !row_ptr || (m > 0 && (!col || !val)))
+    return fail(DAWN_EINVAL, "bad graph arguments (n=%lld, m=%lld)", (long long)n, (long long)m);
+  if (vtype < DAWN_I32 || vtype > DAWN_F64) return fail(DAWN_EINVAL, "unknown vtype %d", vtype);
+  if ((uint64_t)n >= 0xFFFFFFFEull || n >= (1ll << 31))
+    return fail(DAWN_EUNSUPPORTED, "n=%lld exceeds the 2^31 node limit", (long long)n);
+  const int cbits = bitlen((uint64_t)n);
+  if (bitlen((uint64_t)m) >= 64 - cbits)
+    return fail(DAWN_EUNSUPPORTED, "m=%lld too large for the packed frontier reservation", (long long)m);
+  int ndev = 0;
+  CK(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return fail(DAWN_EINVAL, "device %d out of range (%d devices)", device, ndev);
+  CK(cudaSetDevice(device));
+
+  dawn_graph_s* g = new dawn_graph_s();
+  g->device = device;
+  g->n = n;
+  g->m = m;
+  g->vtype = vtype;
+  g->wide = (uint64_t)m > 0xFFFFFFFFull - 4ull * TILE;
+  const size_t eis = g->wide ? 8 : 4;
+  auto cleanup = [&](int rc) { graph_free(g); return rc; };
+  cudaError_t e;
+  if ((e = cudaMalloc(&g->row_ptr, eis * (size_t)(n + 1))) != cudaSuccess)
+    return cleanup(fail(DAWN_ENOMEM, "row_ptr alloc: %s", cudaGetErrorString(e)));
+  g->bytes += eis * (n + 1);
+  const size_t mm = (size_t)std::max<int64_t>(m, 1);
+  if (value_size(vtype) == 4) {
+    if ((e = cudaMalloc(&g->e2, 8 * mm)) != cudaSuccess)
+      return cleanup(fail(DAWN_ENOMEM, "edge alloc: %s", cudaGetErrorString(e)));
+    g->bytes += 8 * mm;
+  } else {
+    if ((e = cudaMalloc(&g->ecol, 4 * mm)) != cudaSuccess ||
+        (e = cudaMalloc(&g->ew, 8 * mm)) != cudaSuccess)
+      return cleanup(fail(DAWN_ENOMEM, "edge alloc: %s", cudaGetErrorString(e)));
+    g->bytes += 12 * mm;
+  }
+
+  // stage the reference-layout arrays on the device if they live on the host
+  const int64_t* d_rp = row_ptr;
+  const int64_t* d_col = col;
+  const double* d_val = val;
+  void* tmp = nullptr;
+  unsigned* d_flags = nullptr;
+  if (!src_is_device) {
+    const size_t bytes = 8 * (size_t)(n + 1) + 16 * (size_t)m;
+    if ((e = cudaMalloc(&tmp, bytes)) != cudaSuccess)
+      return cleanup(fail(DAWN_ENOMEM, "staging alloc: %s", cudaGetErrorString(e)));
+    char* p = (char*)tmp;
+    int64_t* s_rp = (int64_t*)p;
+    int64_t* s_col = (int64_t*)(p + 8 * (n + 1));
+    double* s_val = (double*)(p + 8 * (n + 1) + 8 * m);
+    e = cudaMemcpy(s_rp, row_ptr, 8 * (size_t)(n + 1), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && m) e = cudaMemcpy(s_col, col, 8 * (size_t)m, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && m) e = cudaMemcpy(s_val, val, 8 * (size_t)m, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+      cudaFree(tmp);
+      return cleanup(fail(DAWN_ECUDA, "graph upload: %s", cudaGetErrorString(e)));
+    }
+    d_rp = s_rp;
+    d_col = s_col;
+    d_val = s_val;
+  }
+  if ((e = cudaMalloc(&d_flags, sizeof(unsigned))) != cudaSuccess ||
+      (e = cudaMemset(d_flags, 0, sizeof(unsigned))) != cudaSuccess) {
+    cudaFree(tmp);
+    return cleanup(fail(DAWN_ECUDA, "flags: %s", cudaGetErrorString(e)));
+  }
+  int rc = DAWN_OK;
+  switch (vtype) {
+    case DAWN_I32: rc = convert_graph<int32_t>(g, d_rp, d_col, d_val, d_flags); break;
+    case DAWN_I64: rc = convert_graph<int64_t>(g, d_rp, d_col, d_val, d_flags); break;
+    case DAWN_F32: rc = convert_graph<float>(g, d_rp, d_col, d_val, d_flags); break;
+    default: rc = convert_graph<double>(g, d_rp, d_col, d_val, d_flags); break;
+  }
+  unsigned hflags = 0;
+  if (rc == DAWN_OK) {
+    e = cudaMemcpy(&hflags, d_flags, sizeof(unsigned), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) rc = fail(DAWN_ECUDA, "graph convert: %s", cudaGetErrorString(e));
+  }
+  cudaFree(tmp);
+  cudaFree(d_flags);
+  if (rc != DAWN_OK) return cleanup(rc);
+  if (hflags & ERR_ROWPTR) return cleanup(fail(DAWN_EINVAL, "row_ptr must start at 0, end at m and be monotone"));
+  if (hflags & ERR_COL) return cleanup(fail(DAWN_EINVAL, "column index out of range"));
+  if (hflags & ERR_NONINT) return cleanup(fail(DAWN_EINVAL, "non-integral weight for an integer value type"));
+  if (hflags & ERR_RANGE) return cleanup(fail(DAWN_EINVAL, "weight out of range for the value type"));
+  g->has_negative = (hflags & NEG) != 0;
+  *out = g;
+  return DAWN_OK;
+}
+
+extern "C" int dawn_graph_destroy(dawn_graph_t g) {
+  graph_free(g);
+  return DAWN_OK;
+}
+
+extern "C" int dawn_graph_info(dawn_graph_t g, int64_t* n, int64_t* m, int* vtype,
+                               int64_t* device_bytes) {
+  if (!g) return fail(DAWN_EINVAL, "graph is NULL");
+  if (n) *n = g->n;
+  if (m) *m = g->m;
+  if (vtype) *vtype = g->vtype;
+  if (device_bytes) *device_bytes = g->bytes;
+  return DAWN_OK;
+}
+
+// ---------------------------------------------------------------------------
+// solver
+// ---------------------------------------------------------------------------
+template <class V, class EI>
+struct Impl {
+  using K = typename Val<V>::K;
+
+  static KParams<V, EI> params(dawn_solver_t s, unsigned max_rounds) {
+    dawn_graph_t g = s->g;
+    KParams<V, EI> P;
+    P.n = (uint32_t)g->n;
+    P.src = (uint32_t)s->source;
+    P.row_ptr = (const EI*)g->row_ptr;
+    P.e2 = g->e2;
+    P.ecol = g->ecol;
+    P.ew = g->ew;
+    P.dist = (K*)s->dist;
+    P.stamp = s->stamp;
+    P.pred = s->pred;
+    P.jmp0 = s->jmp0;
+    P.jmp1 = s->jmp1;
+    for (int i = 0; i < 2; ++i) {
+      P.qnode[i] = s->qnode[i];
+      P.qoff[i] = (EI*)s->qoff[i];
+      P.qbase[i] = (EI*)s->qbase[i];
+      P.qkey[i] = (K*)s->qkey[i];
+    }
+    P.tile_row = s->tile_row;
+    P.st = s->st;
+    P.algo = s->algo;
+    const bool neg = (s->run_flags & DAWN_F_NEGCHECK) && g->has_negative &&
+                     (g->vtype == DAWN_I32 || g->vtype == DAWN_I64) && s->pred != nullptr;
+    P.pred_on = ((s->run_flags & DAWN_F_PRED) || neg) ? 1 : 0;
+    P.negcheck_period = neg ? 16 : 0;
+    P.logn = s->logn;
+    P.ebits = s->ebits;
+    P.max_rounds = max_rounds;
+    return P;
+  }
+
+  static size_t smem_bytes() { return sizeof(Smem<V, EI>); }
+
+  static int setup(dawn_solver_t s) {
+    const size_t sm = smem_bytes();
+    CK(cudaFuncSetAttribute(dawn_persistent<V, EI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    int bps = 0, nsm = 0, dev = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, dawn_persistent<V, EI>, NT, sm));
+    if (bps < 1) return fail(DAWN_ECUDA, "persistent kernel cannot be resident (smem %zu)", sm);
+    const int64_t n = s->g->n, m = s->g->m;
+    const int64_t work = std::max<int64_t>((n + TILE - 1) / TILE, (m + TILE - 1) / TILE);
+    s->grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)bps * nsm, work));
+    s->smem = sm;
+    return DAWN_OK;
+  }
+
+  static int begin(dawn_solver_t s, cudaStream_t stream) {
+    const int64_t n = s->g->n;
+    CK(cudaMemsetAsync(s->dist, 0xFF, sizeof(K) * n, stream));
+    CK(cudaMemsetAsync(s->stamp, 0, sizeof(uint32_t) * n, stream));
+    if (s->pred) CK(cudaMemsetAsync(s->pred, 0, sizeof(unsigned long long) * n, stream));
+    KParams<V, EI> P = params(s, 0);
+    dawn_init_solve<V, EI><<<1, 32, 0, stream>>>(P);
+    CK(cudaGetLastError());
+    return DAWN_OK;
+  }
+
+  static int run(dawn_solver_t s, unsigned max_rounds, cudaStream_t stream) {
+    KParams<V, EI> P = params(s, max_rounds);
+    void* args[] = {&P};
+    CK(cudaLaunchCooperativeKernel((void*)dawn_persistent<V, EI>, dim3(s->grid), dim3(NT), args,
+                                   s->smem, stream));
+    return DAWN_OK;
+  }
+
+  static int decode(dawn_solver_t s, double* dist_out, int64_t* pred_out, cudaStream_t stream) {
+    const int64_t n = s->g->n;
+    const int blocks = (int)std::min<int64_t>(148 * 16, (n + 255) / 256);
+    if (dist_out) {
+      const bool dev = is_device_ptr(dist_out);
+      double* target = dev ? dist_out : s->dbuf;
+      dawn_decode_dist<V><<<blocks, 256, 0, stream>>>((const K*)s->dist, (uint32_t)n, target);
+      CK(cudaGetLastError());
+      if (!dev) CK(cudaMemcpyAsync(dist_out, s->dbuf, 8 * (size_t)n, cudaMemcpyDeviceToHost, stream));
+    }
+    if (pred_out) {
+      if (!s->pred) return fail(DAWN_EINVAL, "solver was created without DAWN_F_PRED");
+      const bool dev = is_device_ptr(pred_out);
+      int64_t* target = dev ? pred_out : s->pbuf;
+      dawn_decode_pred<V><<<blocks, 256, 0, stream>>>((const K*)s->dist, s->pred, (uint32_t)n,
+                                                      (uint32_t)s->source, target);
+      CK(cudaGetLastError());
+      if (!dev) CK(cudaMemcpyAsync(pred_out, s->pbuf, 8 * (size_t)n, cudaMemcpyDeviceToHost, stream));
+    }
+    return DAWN_OK;
+  }
+
+  static int alloc(dawn_solver_t s) {
+    const int64_t n = s->g->n, m = s->g->m;
+    const size_t ks = sizeof(K), es = sizeof(EI);
+    CK(cudaMalloc(&s->dist, ks * n));
+    CK(cudaMalloc(&s->stamp, 4 * n));
+    if (s->flags & (DAWN_F_PRED | DAWN_F_NEGCHECK)) {
+      CK(cudaMalloc(&s->pred, 8 * n));
+      CK(cudaMalloc(&s->jmp0, 4 * n));
+      CK(cudaMalloc(&s->jmp1, 4 * n));
+      CK(cudaMalloc(&s->pbuf, 8 * n));
+    }
+    for (int i = 0; i < 2; ++i) {
+      CK(cudaMalloc(&s->qnode[i], 4 * n));
+      CK(cudaMalloc(&s->qoff[i], es * n));
+      CK(cudaMalloc(&s->qbase[i], es * n));
+      CK(cudaMalloc(&s->qkey[i], ks * n));
+    }
+    CK(cudaMalloc(&s->tile_row, 4 * (size_t)(m / TILE + 4)));
+    CK(cudaMalloc(&s->st, sizeof(DevState)));
+    CK(cudaMemset(s->st, 0, sizeof(DevState)));
+    CK(cudaMallocHost(&s->st_host, sizeof(DevState)));
+    CK(cudaMalloc(&s->dbuf, 8 * n));
+    return setup(s);
+  }
+};
+
+#define DISPATCH(g, CALL)                                                         \
+  ([&]() -> int {                                                                 \
+    switch ((g)->vtype) {                                                         \
+      case DAWN_I32:                                                              \
+        return (g)->wide ? Impl<int32_t, unsigned long long>::CALL : Impl<int32_t, uint32_t>::CALL; \
+      case DAWN_I64:                                                              \
+        return (g)->wide ? Impl<int64_t, unsigned long long>::CALL : Impl<int64_t, uint32_t>::CALL; \
+      case DAWN_F32:                                                              \
+        return (g)->wide ? Impl<float, unsigned long long>::CALL : Impl<float, uint32_t>::CALL;     \
+      default:                                                                    \
+        return (g)->wide ? Impl<double, unsigned long long>::CALL : Impl<double, uint32_t>::CALL;   \
+    }                                                                             \
+  }())
+
+static void solver_free(dawn_solver_t s) {
+  if (!s) return;
+  cudaSetDevice(s->g->device);
+  cudaFree(s->dist);
+  cudaFree(s->stamp);
+  cudaFree(s->pred);
+  cudaFree(s->jmp0);
+  cudaFree(s->jmp1);
+  cudaFree(s->pbuf);
+  for (int i = 0; i < 2; ++i) {
+    cudaFree(s->qnode[i]);
+    cudaFree(s->qoff[i]);
+    cudaFree(s->qbase[i]);
+    cudaFree(s->qkey[i]);
+  }
+  cudaFree(s->tile_row);
+  cudaFree(s->st);
+  cudaFreeHost(s->st_host);
+  cudaFree(s->dbuf);
+  delete s;
+}
+
+extern "C" int dawn_solver_create(dawn_graph_t g, unsigned flags, dawn_solver_t* out) {
+  if (!g || !out) return fail(DAWN_EINVAL, "NULL argument");
+  *out = nullptr;
+  CK(cudaSetDevice(g->device));
+  dawn_solver_s* s = new dawn_solver_s();
+  s->g = g;
+  s->flags = flags;
+  s->ebits = 64 - bitlen((uint64_t)g->n);
+  int lg = 0;
+  while ((1ll << lg) < g->n) ++lg;
+  s->logn = lg;
+  int rc = DISPATCH(g, alloc(s));
+  if (rc != DAWN_OK) {
+    solver_free(s);
+    return rc;
+  }
+  *out = s;
+  return DAWN_OK;
+}
+
+extern "C" int dawn_solver_destroy(dawn_solver_t s) {
+  solver_free(s);
+  return DAWN_OK;
+}
+
+static int check_solve_args(dawn_solver_t s, int64_t source, int algo, unsigned flags) {
+  if (!s) return fail(DAWN_EINVAL, "solver is NULL");
+  if (source < 0 || source >= s->g->n)
+    return fail(DAWN_ESOURCE, "source %lld out of range for n=%lld", (long long)source, (long long)s->g->n);
+  if (algo != DAWN_GOVM && algo != DAWN_GSVM) return fail(DAWN_EINVAL, "unknown algo %d", algo);
+  if ((flags & DAWN_F_PRED) && !(s->flags & DAWN_F_PRED))
+    return fail(DAWN_EINVAL, "DAWN_F_PRED requested but the solver was created without it");
+  return DAWN_OK;
+}
+
+static int do_begin(dawn_solver_t s, int64_t source, int algo, unsigned flags, cudaStream_t st) {
+  CK(cudaSetDevice(s->g->device));
+  s->source = source;
+  s->algo = algo;
+  s->run_flags = flags & (s->flags | DAWN_F_NEGCHECK);
+  if ((s->run_flags & DAWN_F_NEGCHECK) && !s->pred) s->run_flags &= ~DAWN_F_NEGCHECK;
+  s->active = true;
+  return DISPATCH(s->g, begin(s, st));
+}
+
+static void fill_stats(const DevState& d, dawn_stats_t* o) {
+  o->outer_steps = (int64_t)d.steps;
+  o->relaxations = (int64_t)d.R;
+  o->writes = (int64_t)d.W;
+  o->first_discoveries = (int64_t)d.FD;
+  o->multi_written = (int64_t)d.multi;
+  o->negative_cycle = d.flag ? 1 : 0;
+  o->early_exit = d.early ? 1 : 0;
+}
+
+static int read_state(dawn_solver_t s, cudaStream_t st) {
+  CK(cudaMemcpyAsync(s->st_host, s->st, sizeof(DevState), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return DAWN_OK;
+}
+
+extern "C" int dawn_sssp(dawn_solver_t s, int64_t source, int algo, unsigned flags,
+                         double* dist_out, int64_t* pred_out, dawn_stats_t* stats_out,
+                         void* stream) {
+  TRY(check_solve_args(s, source, algo, flags));
+  if (pred_out && !(flags & DAWN_F_PRED)) return fail(DAWN_EINVAL, "pred_out requires DAWN_F_PRED");
+  cudaStream_t st = (cudaStream_t)stream;
+  TRY(do_begin(s, source, algo, flags, st));
+  TRY(DISPATCH(s->g, run(s, 0xFFFFFFFFu, st)));
+  TRY(DISPATCH(s->g, decode(s, dist_out, pred_out, st)));
+  if (stats_out) {
+    TRY(read_state(s, st));
+    fill_stats(*s->st_host, stats_out);
+  }
+  return DAWN_OK;
+}
+
+extern "C" int dawn_sssp_begin(dawn_solver_t s, int64_t source, int algo, unsigned flags,
+                               void* stream) {
+  TRY(check_solve_args(s, source, algo, flags));
+  return do_begin(s, source, algo, flags, (cudaStream_t)stream);
+}
+
+extern "C" int dawn_sssp_advance(dawn_solver_t s, int max_rounds, int64_t* round_out,
+                                 int* done_out, void* stream) {
+  if (!s || !s->active) return fail(DAWN_EINVAL, "no active solve");
+  if (max_rounds < 1) return fail(DAWN_EINVAL, "max_rounds must be >= 1");
+  cudaStream_t st = (cudaStream_t)stream;
+  CK(cudaSetDevice(s->g->device));
+  TRY(read_state(s, st));
+  if (!s->st_host->done) {
+    TRY(DISPATCH(s->g, run(s, (unsigned)max_rounds, st)));
+    TRY(read_state(s, st));
+  }
+  if (round_out) *round_out = (int64_t)s->st_host->round - 1;
+  if (done_out) *done_out = s->st_host->done ? 1 : 0;
+  return DAWN_OK;
+}
+
+extern "C" int dawn_sssp_run(dawn_solver_t s, int max_rounds, void* stream) {
+  if (!s || !s->active) return fail(DAWN_EINVAL, "no active solve");
+  if (max_rounds < 0) return fail(DAWN_EINVAL, "max_rounds must be >= 0");
+  CK(cudaSetDevice(s->g->device));
+  return DISPATCH(s->g, run(s, max_rounds == 0 ? 0xFFFFFFFFu : (unsigned)max_rounds, (cudaStream_t)stream));
+}
+
+extern "C" int dawn_solver_state(dawn_solver_t s, double* dist_out, uint32_t* stamp_out,
+                                 void* stream) {
+  if (!s || !s->active) return fail(DAWN_EINVAL, "no active solve");
+  cudaStream_t st = (cudaStream_t)stream;
+  CK(cudaSetDevice(s->g->device));
+  TRY(DISPATCH(s->g, decode(s, dist_out, nullptr, st)));
+  if (stamp_out)
+    CK(cudaMemcpyAsync(stamp_out, s->stamp, 4 * (size_t)s->g->n, cudaMemcpyDefault, st));
+  CK(cudaStreamSynchronize(st));
+  return DAWN_OK;
+}
+
+extern "C" int dawn_solver_result(dawn_solver_t s, double* dist_out, int64_t* pred_out,
+                                  dawn_stats_t* stats_out, void* stream) {
+  if (!s || !s->active) return fail(DAWN_EINVAL, "no solve has run on this solver");
+  cudaStream_t st = (cudaStream_t)stream;
+  CK(cudaSetDevice(s->g->device));
+  if (pred_out && !(s->run_flags & DAWN_F_PRED)) return fail(DAWN_EINVAL, "last solve did not record predecessors");
+  TRY(DISPATCH(s->g, decode(s, dist_out, pred_out, st)));
+  TRY(read_state(s, st));
+  if (stats_out) fill_stats(*s->st_host, stats_out);
+  return DAWN_OK;
+}
+
+extern "C" int dawn_mssp(dawn_solver_t s, const int64_t* sources, int64_t k, int algo,
+                         unsigned flags, double* dist_out, dawn_stats_t* stats_out, void* stream) {
+  if (!s) return fail(DAWN_EINVAL, "solver is NULL");
+  if (k < 0 || (k > 0 && !sources)) return fail(DAWN_EINVAL, "bad sources");
+  for (int64_t i = 0; i < k; ++i) TRY(check_solve_args(s, sources[i], algo, flags & ~DAWN_F_PRED));
+  cudaStream_t st = (cudaStream_t)stream;
+  CK(cudaSetDevice(s->g->device));
+  DevState* hs = nullptr;
+  if (stats_out && k > 0) CK(cudaMallocHost(&hs, sizeof(DevState) * k));
+  const int64_t n = s->g->n;
+  int rc = DAWN_OK;
+  for (int64_t i = 0; i < k && rc == DAWN_OK; ++i) {
+    rc = do_begin(s, sources[i], algo, flags & ~DAWN_F_PRED, st);
+    if (rc == DAWN_OK) rc = DISPATCH(s->g, run(s, 0xFFFFFFFFu, st));
+    if (rc == DAWN_OK && dist_out) rc = DISPATCH(s->g, decode(s, dist_out + i * n, nullptr, st));
+    if (rc == DAWN_OK && hs) {
+      cudaError_t e = cudaMemcpyAsync(hs + i, s->st, sizeof(DevState), cudaMemcpyDeviceToHost, st);
+      if (e != cudaSuccess) rc = fail(DAWN_ECUDA, "stats copy: %s", cudaGetErrorString(e));
+    }
+  }
+  if (rc == DAWN_OK) {
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) rc = fail(DAWN_ECUDA, "mssp: %s", cudaGetErrorString(e));
+  }
+  if (rc == DAWN_OK && hs)
+    for (int64_t i = 0; i < k; ++i) fill_stats(hs[i], stats_out + i);
+  if (hs) cudaFreeHost(hs);
+  return rc;
+}
+
+// ---------------------------------------------------------------------------
+// synthetic RMAT generator (counter-based, see generators.py for the spec)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+__device__ __forceinline__ unsigned long long draw64(unsigned long long seed, unsigned long long i,
+                                                     unsigned lvl) {
+  return mix64(seed * 0x9E3779B97F4A7C15ull + i * 64ull + lvl + 0x9E3779B97F4A7C15ull);
+}
+
+__global__ void k_gen_rmat(int scale, int64_t m, uint32_t A, uint32_t AB, uint32_t ABC,
+                           unsigned long long seed, int wkind, int64_t wlo, unsigned long long wrange,
+                           unsigned long long wseed, int64_t* u_out, int64_t* v_out, double* w_out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t u = 0, v = 0;
+    for (int l = 0; l < scale; ++l) {
+      const uint32_t q = (uint32_t)(draw64(seed, (unsigned long long)i, l) >> 40);
+      const int ub = q >= AB;
+      const int vb = (q >= A && q < AB) || q >= ABC;
+      u |= (int64_t)ub << l;
+      v |= (int64_t)vb << l;
+    }
+    const unsigned long long h = draw64(wseed, (unsigned long long)i, 63);
+    double w;
+    if (wkind == 0) w = (double)(wlo + (int64_t)(((h >> 32) * wrange) >> 32));
+    else w = (double)((float)(h >> 40) * (1.0f / 16777216.0f));
+    u_out[i] = u;
+    v_out[i] = v;
+    w_out[i] = w;
+  }
+}
+
+extern "C" int dawn_gen_rmat(int device, int scale, int64_t edge_factor, double a, double b,
+                             double c, uint64_t seed, int wkind, int64_t wlo, int64_t whi,
+                             uint64_t wseed, int64_t* u_out, int64_t* v_out, double* w_out,
+                             void* stream) {
+  if (scale < 1 || scale > 31 || edge_factor < 1 || !u_out || !v_out || !w_out)
+    return fail(DAWN_EINVAL, "bad rmat arguments");
+  if (wkind == 0 && (whi < wlo || whi - wlo >= (1ll << 32))) return fail(DAWN_EINVAL, "bad weight range");
+  CK(cudaSetDevice(device));
+  const int64_t m = edge_factor << scale;
+  const uint32_t A = (uint32_t)(a * 16777216.0), AB = (uint32_t)((a + b) * 16777216.0),
+                 ABC = (uint32_t)((a + b + c) * 16777216.0);
+  k_gen_rmat<<<148 * 16, 256, 0, (cudaStream_t)stream>>>(scale, m, A, AB, ABC, seed, wkind, wlo,
+                                                        (unsigned long long)(whi - wlo + 1), wseed,
+                                                        u_out, v_out, w_out);
+  CK(cudaGetLastError());
+  return DAWN_OK;
+}

@@ -1,0 +1,451 @@
+"""Drop-in weighted-DAWN solvers on the GPU (mirror of sparsepath/solver.py).
+
+Public names, signatures, return types and error behaviour follow the
+reference (``/root/reference/pkg/src/sparsepath/solver.py``):
+
+  ===================  ==========================  ===============================
+  this module          reference                   device path
+  ===================  ==========================  ===============================
+  ``seed_source``      solver.py:212-250           round 1 of the persistent kernel
+  ``gsvm_sssp``        solver.py:265-321           dawn_sssp(algo=GSVM)
+  ``govm_sssp``        solver.py:324-399           dawn_sssp(algo=GOVM)
+  ``SOLVERS``          solver.py:402               same names
+  ``mssp``             solver.py:426-457           dawn_mssp, sources over GPUs
+  ``apsp``             solver.py:460-495           dawn_mssp in row blocks -> sink
+  ===================  ==========================  ===============================
+
+Semantics.  Distances and the ``negative_cycle`` flag equal the reference's:
+both the reference's in-place (Gauss-Seidel) relaxation and the device's
+frontier-synchronous (snapshot-Jacobi) rounds converge to the same greatest
+fixpoint of ``d[v] = min(d[v], fl(d[u] + w))`` with the source pinned, so
+integer and float64 results are bit-identical.  Work counters are reported
+under snapshot-Jacobi round semantics: deterministic
+across runs, ``workers`` and devices, equal to the reference on its
+known-answer fixtures, but not equal to its Gauss-Seidel counts on large
+graphs.  ``trace`` and ``record_pred`` run a host-synchronised stepping /
+predecessor pass on the device.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+from concurrent.futures import ThreadPoolExecutor
+from ctypes import byref, c_int, c_int64
+from dataclasses import dataclass
+from math import inf
+from typing import Callable, Iterable, Sequence
+
+import numpy as np
+
+from . import _native as N
+from .device import DeviceGraph, device_graph
+
+__all__ = [
+    "DistanceVector",
+    "PredecessorVector",
+    "FrontierFlags",
+    "SolveStats",
+    "AggregateStats",
+    "seed_source",
+    "gsvm_sssp",
+    "govm_sssp",
+    "mssp",
+    "apsp",
+    "aggregate_stats",
+    "format_distance_row",
+    "SOLVERS",
+]
+
+
+# ---------------------------------------------------------------------------
+# result types (reference solver.py:66-209)
+# ---------------------------------------------------------------------------
+@dataclass(frozen=True, eq=False)
+class DistanceVector:
+    """Distances from ``source``; ``inf`` = unreachable (solver.py:66-71)."""
+
+    dist: np.ndarray
+    source: int
+
+
+@dataclass
+class PredecessorVector:
+    """Shortest-path tree witness (solver.py:74-98).
+
+    ``pred[j]`` is a node whose value produced ``dist[j]`` in the round that
+    last lowered ``j`` (the smallest such node id — deterministic; the
+    reference keeps the last writer in CSR order).  ``pred[source]`` is None.
+    """
+
+    pred: list
+    source: int
+
+    def path_to(self, j: int) -> list[int] | None:
+        if j != self.source and self.pred[j] is None:
+            return None
+        path = [j]
+        seen = {j}
+        node = j
+        while node != self.source:
+            node = self.pred[node]
+            if node is None or node in seen:  # broken chain (negative cycle)
+                return None
+            seen.add(node)
+            path.append(node)
+        return path[::-1]
+
+
+@dataclass
+class FrontierFlags:
+    """Alg. 2's two frontier vectors (solver.py:101-115); host-side only."""
+
+    current: list
+    next: list
+
+    @classmethod
+    def empty(cls, n: int) -> "FrontierFlags":
+        return cls(current=[False] * n, next=[False] * n)
+
+
+@dataclass
+class SolveStats:
+    """Per-solve work counters (solver.py:118-149)."""
+
+    outer_steps: int = 0
+    relaxations: int = 0
+    writes: int = 0
+    first_discoveries: int = 0
+    re_updates: int = 0
+    mu: float = 0.0
+    updated_ratio: float = 0.0
+    negative_cycle: bool = False
+
+    def as_dict(self) -> dict:
+        return {
+            "outer_steps": self.outer_steps,
+            "relaxations": self.relaxations,
+            "writes": self.writes,
+            "first_discoveries": self.first_discoveries,
+            "re_updates": self.re_updates,
+            "mu": self.mu,
+            "updated_ratio": self.updated_ratio,
+            "negative_cycle": self.negative_cycle,
+        }
+
+
+@dataclass
+class AggregateStats:
+    """Counters summed over solves; means over sources that reach a node (solver.py:152-202)."""
+
+    sources: int = 0
+    reachable_sources: int = 0
+    outer_steps: int = 0
+    relaxations: int = 0
+    writes: int = 0
+    first_discoveries: int = 0
+    re_updates: int = 0
+    mean_mu: float = 0.0
+    mean_updated_ratio: float = 0.0
+    negative_cycle: bool = False
+
+    def add(self, s: SolveStats) -> None:
+        self.sources += 1
+        self.outer_steps += s.outer_steps
+        self.relaxations += s.relaxations
+        self.writes += s.writes
+        self.first_discoveries += s.first_discoveries
+        self.re_updates += s.re_updates
+        self.negative_cycle = self.negative_cycle or bool(s.negative_cycle)
+        if s.first_discoveries > 0:
+            self.reachable_sources += 1
+            self.mean_mu += s.mu  # running sums until finish()
+            self.mean_updated_ratio += s.updated_ratio
+
+    def finish(self) -> "AggregateStats":
+        if self.reachable_sources:
+            self.mean_mu /= self.reachable_sources
+            self.mean_updated_ratio /= self.reachable_sources
+        return self
+
+    def as_dict(self) -> dict:
+        return {
+            "sources": self.sources,
+            "reachable_sources": self.reachable_sources,
+            "outer_steps": self.outer_steps,
+            "relaxations": self.relaxations,
+            "writes": self.writes,
+            "first_discoveries": self.first_discoveries,
+            "re_updates": self.re_updates,
+            "mean_mu": self.mean_mu,
+            "mean_updated_ratio": self.mean_updated_ratio,
+            "negative_cycle": self.negative_cycle,
+        }
+
+
+def aggregate_stats(stats: Iterable[SolveStats]) -> AggregateStats:
+    agg = AggregateStats()
+    for s in stats:
+        agg.add(s)
+    return agg.finish()
+
+
+def _stats_from_native(st: N.Stats) -> SolveStats:
+    """``_finalize`` (solver.py:258-262) over the device counters."""
+    w, fd = int(st.writes), int(st.first_discoveries)
+    denom = max(fd, 1)
+    return SolveStats(
+        outer_steps=int(st.outer_steps),
+        relaxations=int(st.relaxations),
+        writes=w,
+        first_discoveries=fd,
+        re_updates=w - fd,
+        mu=w / denom,
+        updated_ratio=int(st.multi_written) / denom,
+        negative_cycle=bool(st.negative_cycle),
+    )
+
+
+# ---------------------------------------------------------------------------
+# argument checks (same messages as the reference)
+# ---------------------------------------------------------------------------
+def _check_source(g, source: int) -> None:
+    if not 0 <= source < g.n:
+        raise ValueError(f"source {source} out of range for n={g.n}")
+
+
+def _normalize_algo(algo: str) -> str:
+    name = algo.lower()
+    if name not in SOLVERS:
+        raise ValueError(f"unknown solver {algo!r}; expected one of {sorted(SOLVERS)}")
+    return name
+
+
+_ALGO = {"govm": N.GOVM, "gsvm": N.GSVM}
+
+
+def _neg_flags(dg: DeviceGraph) -> int:
+    # integer graphs with negative edges: predecessor-graph cycle check gives
+    # the cap's verdict early (DESIGN.md §Negative cycles)
+    return N.F_NEGCHECK if dg.vtype in (N.I32, N.I64) else 0
+
+
+# ---------------------------------------------------------------------------
+# single-source solves
+# ---------------------------------------------------------------------------
+def _solve(g, source: int, algo: int, record_pred: bool, precision: str | None):
+    _check_source(g, int(source))
+    dg = device_graph(g, precision=precision)
+    flags = (N.F_PRED if record_pred else 0) | _neg_flags(dg)
+    with dg.lock:
+        s = dg.solver(flags)
+        dist = np.empty(dg.n, dtype=np.float64)
+        pred = np.empty(dg.n, dtype=np.int64) if record_pred else None
+        st = N.Stats()
+        N.check(N.lib().dawn_sssp(s, int(source), algo, flags, dist.ctypes.data,
+                                  pred.ctypes.data if pred is not None else None, byref(st), dg.stream()))
+    dv = DistanceVector(dist=dist, source=int(source))
+    pv = None
+    if record_pred:
+        pv = PredecessorVector(pred=[None if p < 0 else int(p) for p in pred.tolist()], source=int(source))
+    return dv, pv, _stats_from_native(st)
+
+
+def _solve_traced(g, source: int, algo: int, record_pred: bool, trace, precision: str | None):
+    """Host-synchronised stepping for the ``trace`` hook (solver.py:328-336, :386-387).
+
+    ``scanned`` for round r is the set lowered in round r-1 and ``written`` the
+    set lowered in round r, both ascending — the write stamps on the device
+    record the last round that lowered each node.
+    """
+    _check_source(g, int(source))
+    dg = device_graph(g, precision=precision)
+    flags = (N.F_PRED if record_pred else 0) | _neg_flags(dg)
+    L = N.lib()
+    with dg.lock:
+        s = dg.solver(flags)
+        stream = dg.stream()
+        n = dg.n
+        dist = np.empty(n, dtype=np.float64)
+        stamp = np.empty(n, dtype=np.uint32)
+        rnd, done = c_int64(0), c_int(0)
+        N.check(L.dawn_sssp_begin(s, int(source), algo, flags, stream))
+        N.check(L.dawn_sssp_advance(s, 1, byref(rnd), byref(done), stream))  # seeding round
+        N.check(L.dawn_solver_state(s, None, stamp.ctypes.data, stream))
+        prev_written = np.flatnonzero((stamp >> 1) == 1).tolist()
+        last = rnd.value
+        while True:
+            N.check(L.dawn_sssp_advance(s, 1, byref(rnd), byref(done), stream))
+            if rnd.value == last:
+                break
+            last = rnd.value
+            N.check(L.dawn_solver_state(s, dist.ctypes.data, stamp.ctypes.data, stream))
+            written = np.flatnonzero((stamp >> 1) == last).tolist()
+            trace(int(last), prev_written, written, dist.tolist())
+            prev_written = written
+        dist_out = np.empty(n, dtype=np.float64)
+        pred = np.empty(n, dtype=np.int64) if record_pred else None
+        st = N.Stats()
+        N.check(L.dawn_solver_result(s, dist_out.ctypes.data, pred.ctypes.data if pred is not None else None,
+                                     byref(st), stream))
+    dv = DistanceVector(dist=dist_out, source=int(source))
+    pv = None
+    if record_pred:
+        pv = PredecessorVector(pred=[None if p < 0 else int(p) for p in pred.tolist()], source=int(source))
+    return dv, pv, _stats_from_native(st)
+
+
+def gsvm_sssp(g, source: int, record_pred: bool = False, *, precision: str | None = None):
+    """Full-rescan SSSP (Alg. 1; reference solver.py:265-321) on the GPU.
+
+    Returns ``(DistanceVector, PredecessorVector | None, SolveStats)``.
+    ``precision`` (extension): ``auto``/``fp32``/``fp64``, default from
+    :func:`set_default_precision`.
+    """
+    return _solve(g, source, N.GSVM, record_pred, precision)
+
+
+def govm_sssp(g, source: int, record_pred: bool = False, trace: Callable | None = None, *,
+              precision: str | None = None):
+    """Frontier SSSP (Alg. 2; reference solver.py:324-399) on the GPU.
+
+    ``trace(step, scanned_nodes, written_nodes, distance_snapshot)`` is called
+    after every round from step 2 on, as in the reference.
+    """
+    if trace is not None:
+        return _solve_traced(g, source, N.GOVM, record_pred, trace, precision)
+    return _solve(g, source, N.GOVM, record_pred, precision)
+
+
+def seed_source(g, source: int, alpha: list, delta: list, stats: SolveStats | None = None,
+                pred: list | None = None, write_counts: list | None = None):
+    """Round 1 of a solve (reference solver.py:212-250), executed on the device.
+
+    Expects ``alpha`` all-infinite except ``alpha[source] == 0`` and ``delta``
+    all-false; updates them in place and returns ``(alpha, delta)``.
+    """
+    _check_source(g, int(source))
+    dg = device_graph(g)
+    L = N.lib()
+    n = dg.n
+    with dg.lock:
+        s = dg.solver(0)
+        stream = dg.stream()
+        rnd, done = c_int64(0), c_int(0)
+        N.check(L.dawn_sssp_begin(s, int(source), N.GOVM, 0, stream))
+        N.check(L.dawn_sssp_advance(s, 1, byref(rnd), byref(done), stream))
+        dist = np.empty(n, dtype=np.float64)
+        stamp = np.empty(n, dtype=np.uint32)
+        N.check(L.dawn_solver_state(s, dist.ctypes.data, stamp.ctypes.data, stream))
+        st = N.Stats()
+        N.check(L.dawn_solver_result(s, None, None, byref(st), stream))
+    written = np.flatnonzero((stamp >> 1) == 1).tolist()
+    for j in written:
+        was_inf = alpha[j] == inf
+        alpha[j] = float(dist[j])
+        delta[j] = True
+        if write_counts is not None:
+            write_counts[j] += 1
+        if pred is not None:
+            pred[j] = int(source)
+        if stats is not None:
+            stats.writes += 1
+            if was_inf:
+                stats.first_discoveries += 1
+    if stats is not None:
+        stats.relaxations += int(st.relaxations)
+        if st.negative_cycle:
+            stats.negative_cycle = True
+    return alpha, delta
+
+
+SOLVERS = {"gsvm": gsvm_sssp, "govm": govm_sssp}
+
+
+# ---------------------------------------------------------------------------
+# multi-source drivers
+# ---------------------------------------------------------------------------
+_ROW_BYTES_BUDGET = 1 << 30  # float64 rows copied back per dawn_mssp call
+
+
+def _mssp_on_device(g, sources: list[int], algo: int, device: int, precision: str | None):
+    dg = device_graph(g, device=device, precision=precision)
+    flags = _neg_flags(dg)
+    n = dg.n
+    rows = np.empty((len(sources), n), dtype=np.float64)
+    stats = (N.Stats * max(len(sources), 1))()
+    chunk = max(1, _ROW_BYTES_BUDGET // (8 * max(n, 1)))
+    with dg.lock:
+        s = dg.solver(flags)
+        for lo in range(0, len(sources), chunk):
+            part = np.asarray(sources[lo:lo + chunk], dtype=np.int64)
+            k = int(part.shape[0])
+            N.check(N.lib().dawn_mssp(s, part.ctypes.data, k, algo, flags, rows[lo:lo + k].ctypes.data,
+                                      ctypes.addressof(stats) + lo * ctypes.sizeof(N.Stats), dg.stream()))
+    return [(DistanceVector(dist=rows[i], source=int(src)), _stats_from_native(stats[i]))
+            for i, src in enumerate(sources)]
+
+
+def _devices_for(workers: int) -> list[int]:
+    ndev = N.device_count()
+    if ndev < 1:
+        N.require_gpu()
+    return list(range(min(max(workers, 1), ndev)))
+
+
+def mssp(g, sources: Sequence[int], algo: str = "govm", workers: int = 1, *,
+         precision: str | None = None) -> list[tuple[DistanceVector, SolveStats]]:
+    """Independent solves from each source, results in the given order (solver.py:426-457).
+
+    ``workers`` is the number of GPUs the sources are spread over (capped at
+    the visible device count); results are bit-identical for any value.
+    """
+    name = _normalize_algo(algo)
+    if workers < 1:
+        raise ValueError("workers must be >= 1")
+    sources = [int(s) for s in sources]
+    for s in sources:
+        _check_source(g, s)
+    if not sources:
+        return []
+    algo_id = _ALGO[name]
+    devs = _devices_for(workers)
+    if len(devs) == 1 or len(sources) == 1:
+        return _mssp_on_device(g, sources, algo_id, devs[0], precision)
+    # contiguous blocks, one host thread per GPU; order restored by block index
+    blocks = np.array_split(np.arange(len(sources)), len(devs))
+    with ThreadPoolExecutor(max_workers=len(devs)) as ex:
+        futs = [ex.submit(_mssp_on_device, g, [sources[i] for i in blk], algo_id, d, precision)
+                for d, blk in zip(devs, blocks) if len(blk)]
+        out = []
+        for f in futs:
+            out.extend(f.result())
+    return out
+
+
+def apsp(g, algo: str = "govm", workers: int = 1, sink: Callable[[DistanceVector], None] | None = None, *,
+         precision: str | None = None) -> AggregateStats:
+    """Every source in ascending order, rows streamed to ``sink`` (solver.py:460-495).
+
+    Rows are produced in device batches and handed to ``sink`` strictly in
+    source order; the n x n matrix is never held.  A sink exception aborts.
+    """
+    name = _normalize_algo(algo)
+    if workers < 1:
+        raise ValueError("workers must be >= 1")
+    agg = AggregateStats()
+    n = g.n
+    if n == 0:
+        return agg.finish()
+    batch = max(1, min(n, (256 << 20) // (8 * n)))
+    for lo in range(0, n, batch):
+        for dv, st in mssp(g, range(lo, min(n, lo + batch)), name, workers, precision=precision):
+            if sink is not None:
+                sink(dv)
+            agg.add(st)
+    return agg.finish()
+
+
+def format_distance_row(dv: DistanceVector) -> str:
+    """``source,d0,d1,...`` with ``%.17g`` and the literal ``inf`` (solver.py:498-506)."""
+    return ",".join([str(dv.source)] + ["inf" if d == inf else "%.17g" % d for d in dv.dist.tolist()])

@@ -1,0 +1,109 @@
+"""Host-side logic that needs no GPU: argument checks in the reference's order,
+containers, generators, stats arithmetic."""
+
+from __future__ import annotations
+
+from math import inf
+
+import numpy as np
+import pytest
+from conftest import make_csr
+
+import paper_2306_07872_b200 as P
+from paper_2306_07872_b200 import generators as G
+
+
+def test_source_checked_before_any_device_work(monkeypatch):
+    g = make_csr(3, [(0, 1, 1.0)])
+    # would raise RuntimeError if it got as far as the device
+    with pytest.raises(ValueError, match="out of range"):
+        P.govm_sssp(g, 3)
+    with pytest.raises(ValueError, match="out of range"):
+        P.gsvm_sssp(g, -1)
+    with pytest.raises(ValueError, match="out of range"):
+        P.mssp(g, [0, 7], "govm")
+    with pytest.raises(ValueError, match="unknown solver"):
+        P.mssp(g, [0], "dijkstra")
+    with pytest.raises(ValueError, match="workers must be >= 1"):
+        P.mssp(g, [0], "govm", workers=0)
+    with pytest.raises(ValueError, match="unknown solver"):
+        P.apsp(g, "bfs")
+
+
+def test_no_cpu_fallback_without_gpu():
+    from paper_2306_07872_b200 import _native as N
+
+    if N.LIB_PATH.exists() and N.device_count() > 0:
+        pytest.skip("a GPU is present")
+    g = make_csr(3, [(0, 1, 1.0)])
+    with pytest.raises(RuntimeError):
+        P.govm_sssp(g, 0)
+
+
+def test_csr_canonical_order_and_validation():
+    g = make_csr(3, [(1, 2, 5.0), (0, 2, 1.0), (0, 1, 2.0), (0, 1, 0.5)])
+    assert g.row_ptr.tolist() == [0, 3, 4, 4]
+    assert g.col.tolist() == [1, 1, 2, 2]
+    assert g.val.tolist() == [2.0, 0.5, 1.0, 5.0]  # ties keep input order
+    assert not g.col.flags.writeable
+    with pytest.raises(ValueError):
+        P.CsrGraph(n=2, m=1, row_ptr=[0, 1, 0], col=[1], val=[1.0])
+    with pytest.raises(ValueError):
+        P.CsrGraph(n=2, m=1, row_ptr=[0, 1, 1], col=[5], val=[1.0])
+    with pytest.raises(ValueError):
+        P.CsrGraph(n=2, m=1, row_ptr=[0, 1, 1], col=[1], val=[np.inf])
+    with pytest.raises(ValueError):
+        P.build_csr(P.EdgeList(n=2, edges=[(0, 3, 1.0)]))
+    rebuilt = P.build_csr(P.to_edge_list(g))
+    assert rebuilt.col.tolist() == g.col.tolist() and rebuilt.val.tolist() == g.val.tolist()
+
+
+def test_generate_random_graph_deterministic():
+    a = P.generate_random_graph(50, 4.0, P.WeightMode.unit(), seed=3)
+    b = P.generate_random_graph(50, 4.0, P.WeightMode.unit(), seed=3)
+    assert a.col.tolist() == b.col.tolist()
+    u = np.repeat(np.arange(a.n), np.diff(a.row_ptr))
+    assert not np.any(u == a.col)  # no self loops
+    w = P.apply_weight_mode(a, P.WeightMode.random_uniform(0, 2, 1))
+    assert w.val.min() >= 0 and w.val.max() < 2
+
+
+def test_grid_generator_shape():
+    g = G.grid_graph(3, 4)
+    assert g.n == 12 and g.m == 2 * (3 * 3 + 2 * 4)
+    assert g.col[g.row_ptr[5]:g.row_ptr[6]].tolist() == [1, 4, 6, 9]
+    assert g.val.min() >= 1 and g.val.max() <= 100
+
+
+def test_rmat_generator_shape():
+    g = G.rmat_graph(10, 8)
+    assert g.n == 1024 and g.m == 8192
+    assert g.out_degree(0) == max(g.out_degree(u) for u in range(g.n))  # vertex 0 is the hub
+
+
+def test_johnson_has_negative_edges_no_cycles():
+    base = G.rmat_graph(8, 4)
+    g, p = G.johnson_reweight(base)
+    assert g.val.min() < 0
+    u = np.repeat(np.arange(g.n), np.diff(g.row_ptr))
+    assert np.allclose(g.val - p[u] + p[g.col], base.val)
+
+
+def test_stats_helpers():
+    s1 = P.SolveStats(writes=3, first_discoveries=2, re_updates=1, mu=1.5, updated_ratio=0.5)
+    s2 = P.SolveStats()
+    agg = P.aggregate_stats([s1, s2])
+    assert agg.sources == 2 and agg.reachable_sources == 1 and agg.mean_mu == 1.5
+    d = s1.as_dict()
+    assert set(map(type, d.values())) <= {int, float, bool}
+    dv = P.DistanceVector(dist=np.array([0.0, 0.1, inf]), source=0)
+    assert P.format_distance_row(dv) == "0,0,0.10000000000000001,inf"
+
+
+def test_path_to():
+    pv = P.PredecessorVector(pred=[None, 0, 1, None], source=0)
+    assert pv.path_to(2) == [0, 1, 2]
+    assert pv.path_to(0) == [0]
+    assert pv.path_to(3) is None
+    loop = P.PredecessorVector(pred=[None, 2, 1], source=0)
+    assert loop.path_to(1) is None
