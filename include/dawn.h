@@ -61,6 +61,7 @@ extern "C" {
 #define DAWN_F_PRED 1u        /* record predecessors (record_pred=True, solver.py:309-310, :383-384) */
 #define DAWN_F_NEGCHECK 2u    /* early negative-cycle exit via predecessor-graph cycle check
                                  (integer types only; same verdict as the n-round cap, solver.py:394-395) */
+#define DAWN_F_PROFILE 4u     /* solver flag: record a per-round device timeline (globaltimer) */
 
 typedef struct dawn_graph_s* dawn_graph_t;
 typedef struct dawn_solver_s* dawn_solver_t;
@@ -106,6 +107,11 @@ int dawn_graph_info(dawn_graph_t g, int64_t* n, int64_t* m, int* vtype, int64_t*
  * predecessor arrays. */
 int dawn_solver_create(dawn_graph_t g, unsigned flags, dawn_solver_t* out);
 int dawn_solver_destroy(dawn_solver_t s);
+/* Tuning knobs (results never depend on them):
+ *   "dense_edges_per_node" (default 0.5): a round that relaxes at least
+ *   value*n edges records its writes as plain stamps and the next frontier is
+ *   rebuilt by a coalesced sweep; lighter rounds enqueue written nodes. */
+int dawn_solver_tune(dawn_solver_t s, const char* key, double value);
 
 /* One single-source solve: govm_sssp / gsvm_sssp (solver.py:265-399),
  * including the seeding round seed_source (solver.py:212-250).
@@ -131,13 +137,21 @@ int dawn_sssp_advance(dawn_solver_t s, int max_rounds, int64_t* round_out, int* 
  * dawn_sssp_begin.  Used to time the persistent kernel alone. */
 int dawn_sssp_run(dawn_solver_t s, int max_rounds, void* stream);
 /* Copy out the current state: dist (float64[n]) and the per-node write stamp
- * (uint32[n]: stamp>>1 = last round that lowered the node, bit0 = lowered in
- * >= 2 rounds).  Any pointer may be NULL.  Synchronises `stream`. */
+ * (uint32[n]: the last round that lowered the node, 0 = never).  Any pointer
+ * may be NULL.  Synchronises `stream`. */
 int dawn_solver_state(dawn_solver_t s, double* dist_out, uint32_t* stamp_out, void* stream);
 /* Result of the last solve on this solver (after dawn_sssp with NULL
  * outputs, or after stepping finished). Synchronises `stream`. */
 int dawn_solver_result(dawn_solver_t s, double* dist_out, int64_t* pred_out,
                        dawn_stats_t* stats_out, void* stream);
+
+/* Per-round timeline of the last solve (solver created with DAWN_F_PROFILE):
+ * 4 uint64 per round r (index r = round number, row 0 unused):
+ *   [0] S-phase start ns, [1] X-phase start ns, [2] round end ns,
+ *   [3] frontier reservation word (entries << ebits | edges).
+ * Copies min(cap_rounds, rounds run + 1) rows; *nrounds = rows available. */
+int dawn_solver_round_profile(dawn_solver_t s, uint64_t* out, int64_t cap_rounds, int64_t* nrounds,
+                              void* stream);
 
 /* Multi-source: independent solves from sources[0..k) (host int64 array) in
  * the given order — mssp (solver.py:426-457).  dist_out is a row-major

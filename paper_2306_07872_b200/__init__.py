@@ -6,7 +6,7 @@ hand-written sm_100a CUDA kernels behind the C ABI in ``include/dawn.h``
 (``libdawn.so``, loaded through ctypes).  There is no CPU fallback.
 """
 
-from .device import DeviceGraph, clear_cache, device_graph, get_default_precision, set_default_precision
+from .device import DeviceGraph, clear_cache, device_graph, get_default_precision, set_default_precision, set_tuning
 from .graph import (
     CsrGraph,
     EdgeList,
@@ -62,4 +62,5 @@ __all__ = [
     "clear_cache",
     "set_default_precision",
     "get_default_precision",
+    "set_tuning",
 ]

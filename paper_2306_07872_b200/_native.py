@@ -13,7 +13,10 @@ import threading
 from ctypes import POINTER, c_char_p, c_double, c_int, c_int32, c_int64, c_uint, c_uint32, c_uint64, c_void_p
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().with_name("libdawn.so")
+import os
+
+# DAWN_LIB: developer override to load an alternative build (tuning variants)
+LIB_PATH = Path(os.environ.get("DAWN_LIB") or Path(__file__).resolve().with_name("libdawn.so"))
 
 DAWN_OK = 0
 DAWN_EINVAL = 1
@@ -29,6 +32,7 @@ PRECISIONS = {"auto": PREC_AUTO, "exact": PREC_AUTO, "fp32": PREC_FP32, "fp64": 
 GOVM, GSVM = 0, 1
 F_PRED = 1
 F_NEGCHECK = 2
+F_PROFILE = 4
 
 # every symbol include/dawn.h declares (checked by tests/test_abi.py)
 EXPORTS = (
@@ -41,12 +45,14 @@ EXPORTS = (
     "dawn_graph_info",
     "dawn_solver_create",
     "dawn_solver_destroy",
+    "dawn_solver_tune",
     "dawn_sssp",
     "dawn_sssp_begin",
     "dawn_sssp_advance",
     "dawn_sssp_run",
     "dawn_solver_state",
     "dawn_solver_result",
+    "dawn_solver_round_profile",
     "dawn_mssp",
     "dawn_gen_rmat",
 )
@@ -83,12 +89,14 @@ def _declare(L: ctypes.CDLL) -> None:
         "dawn_graph_info": (c_int, [c_void_p, P64, P64, POINTER(c_int), P64]),
         "dawn_solver_create": (c_int, [c_void_p, c_uint, POINTER(c_void_p)]),
         "dawn_solver_destroy": (c_int, [c_void_p]),
+        "dawn_solver_tune": (c_int, [c_void_p, c_char_p, c_double]),
         "dawn_sssp": (c_int, [c_void_p, c_int64, c_int, c_uint, c_void_p, c_void_p, POINTER(Stats), c_void_p]),
         "dawn_sssp_begin": (c_int, [c_void_p, c_int64, c_int, c_uint, c_void_p]),
         "dawn_sssp_advance": (c_int, [c_void_p, c_int, P64, POINTER(c_int), c_void_p]),
         "dawn_sssp_run": (c_int, [c_void_p, c_int, c_void_p]),
         "dawn_solver_state": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
         "dawn_solver_result": (c_int, [c_void_p, c_void_p, c_void_p, POINTER(Stats), c_void_p]),
+        "dawn_solver_round_profile": (c_int, [c_void_p, c_void_p, c_int64, P64, c_void_p]),
         "dawn_mssp": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_uint, c_void_p, c_void_p, c_void_p]),
         "dawn_gen_rmat": (c_int, [c_int, c_int, c_int64, c_double, c_double, c_double, c_uint64, c_int,
                                   c_int64, c_int64, c_uint64, c_void_p, c_void_p, c_void_p, c_void_p]),

@@ -76,6 +76,7 @@ struct dawn_solver_s {
   unsigned flags = 0;
   void* dist = nullptr;
   uint32_t* stamp = nullptr;
+  uint8_t* wstate = nullptr;
   unsigned long long* pred = nullptr;
   uint32_t* jmp0 = nullptr;
   uint32_t* jmp1 = nullptr;
@@ -88,8 +89,12 @@ struct dawn_solver_s {
   DevState* st_host = nullptr;  // pinned
   double* dbuf = nullptr;
   int64_t* pbuf = nullptr;
-  int grid = 1;
+  unsigned long long* prof = nullptr;  // per-round timeline (DAWN_F_PROFILE)
+  unsigned prof_cap = 0;
+  int grid = 1;       // co-resident CTAs of the plain persistent kernel
+  int grid_pred = 1;  // ... of the predecessor-tracking instance
   size_t smem = 0;
+  double dense_edges_per_node = 0.5;  // tunable: dense frontier build after rounds relaxing >= this * n edges
   int ebits = 32;
   int logn = 0;
   // current solve
@@ -372,6 +377,7 @@ struct Impl {
     P.ew = g->ew;
     P.dist = (K*)s->dist;
     P.stamp = s->stamp;
+    P.wstate = s->wstate;
     P.pred = s->pred;
     P.jmp0 = s->jmp0;
     P.jmp1 = s->jmp1;
@@ -391,6 +397,9 @@ struct Impl {
     P.logn = s->logn;
     P.ebits = s->ebits;
     P.max_rounds = max_rounds;
+    P.dense_edges = (unsigned long long)std::max(1.0, s->dense_edges_per_node * (double)g->n);
+    P.prof = s->prof;
+    P.prof_cap = s->prof_cap;
     return P;
   }
 
@@ -398,15 +407,18 @@ struct Impl {
 
   static int setup(dawn_solver_t s) {
     const size_t sm = smem_bytes();
-    CK(cudaFuncSetAttribute(dawn_persistent<V, EI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    int bps = 0, nsm = 0, dev = 0;
+    CK(cudaFuncSetAttribute(dawn_persistent<V, EI, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    CK(cudaFuncSetAttribute(dawn_persistent<V, EI, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    int bps0 = 0, bps1 = 0, nsm = 0, dev = 0;
     CK(cudaGetDevice(&dev));
     CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, dawn_persistent<V, EI>, NT, sm));
-    if (bps < 1) return fail(DAWN_ECUDA, "persistent kernel cannot be resident (smem %zu)", sm);
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps0, dawn_persistent<V, EI, false>, NT, sm));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps1, dawn_persistent<V, EI, true>, NT, sm));
+    if (bps0 < 1 || bps1 < 1) return fail(DAWN_ECUDA, "persistent kernel cannot be resident (smem %zu)", sm);
     const int64_t n = s->g->n, m = s->g->m;
     const int64_t work = std::max<int64_t>((n + TILE - 1) / TILE, (m + TILE - 1) / TILE);
-    s->grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)bps * nsm, work));
+    s->grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)bps0 * nsm, work));
+    s->grid_pred = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)bps1 * nsm, work));
     s->smem = sm;
     return DAWN_OK;
   }
@@ -415,6 +427,8 @@ struct Impl {
     const int64_t n = s->g->n;
     CK(cudaMemsetAsync(s->dist, 0xFF, sizeof(K) * n, stream));
     CK(cudaMemsetAsync(s->stamp, 0, sizeof(uint32_t) * n, stream));
+    CK(cudaMemsetAsync(s->wstate, 0, (size_t)n, stream));
+    if (s->prof) CK(cudaMemsetAsync(s->prof, 0, 32 * (size_t)s->prof_cap, stream));
     if (s->pred) CK(cudaMemsetAsync(s->pred, 0, sizeof(unsigned long long) * n, stream));
     KParams<V, EI> P = params(s, 0);
     dawn_init_solve<V, EI><<<1, 32, 0, stream>>>(P);
@@ -425,8 +439,13 @@ struct Impl {
   static int run(dawn_solver_t s, unsigned max_rounds, cudaStream_t stream) {
     KParams<V, EI> P = params(s, max_rounds);
     void* args[] = {&P};
-    CK(cudaLaunchCooperativeKernel((void*)dawn_persistent<V, EI>, dim3(s->grid), dim3(NT), args,
-                                   s->smem, stream));
+    if (P.pred_on) {
+      CK(cudaLaunchCooperativeKernel((void*)dawn_persistent<V, EI, true>, dim3(s->grid_pred), dim3(NT), args,
+                                     s->smem, stream));
+    } else {
+      CK(cudaLaunchCooperativeKernel((void*)dawn_persistent<V, EI, false>, dim3(s->grid), dim3(NT), args,
+                                     s->smem, stream));
+    }
     return DAWN_OK;
   }
 
@@ -457,6 +476,7 @@ struct Impl {
     const size_t ks = sizeof(K), es = sizeof(EI);
     CK(cudaMalloc(&s->dist, ks * n));
     CK(cudaMalloc(&s->stamp, 4 * n));
+    CK(cudaMalloc(&s->wstate, (size_t)n));
     if (s->flags & (DAWN_F_PRED | DAWN_F_NEGCHECK)) {
       CK(cudaMalloc(&s->pred, 8 * n));
       CK(cudaMalloc(&s->jmp0, 4 * n));
@@ -474,6 +494,10 @@ struct Impl {
     CK(cudaMemset(s->st, 0, sizeof(DevState)));
     CK(cudaMallocHost(&s->st_host, sizeof(DevState)));
     CK(cudaMalloc(&s->dbuf, 8 * n));
+    if (s->flags & DAWN_F_PROFILE) {
+      s->prof_cap = 1u << 16;
+      CK(cudaMalloc(&s->prof, 32 * (size_t)s->prof_cap));
+    }
     return setup(s);
   }
 };
@@ -497,6 +521,7 @@ static void solver_free(dawn_solver_t s) {
   cudaSetDevice(s->g->device);
   cudaFree(s->dist);
   cudaFree(s->stamp);
+  cudaFree(s->wstate);
   cudaFree(s->pred);
   cudaFree(s->jmp0);
   cudaFree(s->jmp1);
@@ -511,6 +536,7 @@ static void solver_free(dawn_solver_t s) {
   cudaFree(s->st);
   cudaFreeHost(s->st_host);
   cudaFree(s->dbuf);
+  cudaFree(s->prof);
   delete s;
 }
 
@@ -532,6 +558,16 @@ extern "C" int dawn_solver_create(dawn_graph_t g, unsigned flags, dawn_solver_t*
   }
   *out = s;
   return DAWN_OK;
+}
+
+extern "C" int dawn_solver_tune(dawn_solver_t s, const char* key, double value) {
+  if (!s || !key) return fail(DAWN_EINVAL, "NULL argument");
+  if (!strcmp(key, "dense_edges_per_node")) {
+    if (!(value >= 0.0)) return fail(DAWN_EINVAL, "dense_edges_per_node must be >= 0");
+    s->dense_edges_per_node = value;
+    return DAWN_OK;
+  }
+  return fail(DAWN_EINVAL, "unknown tuning key '%s'", key);
 }
 
 extern "C" int dawn_solver_destroy(dawn_solver_t s) {
@@ -641,6 +677,20 @@ extern "C" int dawn_solver_result(dawn_solver_t s, double* dist_out, int64_t* pr
   TRY(DISPATCH(s->g, decode(s, dist_out, pred_out, st)));
   TRY(read_state(s, st));
   if (stats_out) fill_stats(*s->st_host, stats_out);
+  return DAWN_OK;
+}
+
+extern "C" int dawn_solver_round_profile(dawn_solver_t s, uint64_t* out, int64_t cap_rounds,
+                                         int64_t* nrounds, void* stream) {
+  if (!s || !s->active) return fail(DAWN_EINVAL, "no solve has run on this solver");
+  if (!s->prof) return fail(DAWN_EINVAL, "solver was created without DAWN_F_PROFILE");
+  cudaStream_t st = (cudaStream_t)stream;
+  CK(cudaSetDevice(s->g->device));
+  TRY(read_state(s, st));
+  const int64_t done = std::min<int64_t>((int64_t)s->st_host->round, (int64_t)s->prof_cap);
+  const int64_t k = std::min<int64_t>(done, cap_rounds);
+  if (out && k > 0) CK(cudaMemcpy(out, s->prof, 32 * (size_t)k, cudaMemcpyDeviceToHost));
+  if (nrounds) *nrounds = done;
   return DAWN_OK;
 }
 

@@ -11,7 +11,14 @@
 
 namespace dawn {
 
-constexpr int NT = 256;             // threads per CTA
+#ifndef DAWN_MIN_BLOCKS
+#define DAWN_MIN_BLOCKS 3   // resident CTAs per SM the register budget is sized for
+#endif
+
+#ifndef DAWN_NT
+#define DAWN_NT 256
+#endif
+constexpr int NT = DAWN_NT;         // threads per CTA
 constexpr int ITEMS = 8;            // virtual edges per thread per tile
 constexpr int TILE = NT * ITEMS;    // virtual edges per tile (2048)
 
@@ -201,6 +208,8 @@ struct DevState {
   unsigned tile_ctr2[2];         // dynamic tile counters (predecessor pass)
   unsigned bar;                  // grid barrier word (never reset)
   unsigned round;                // next round to run (1 = seeding round)
+  unsigned dense_prev;           // round-1 recorded its writes densely (stamps only)
+  unsigned resume_x;             // stepping: the frontier of `round` is built, resume at its X phase
   unsigned done;
   unsigned flag;                 // negative cycle
   unsigned early;                // stopped by the predecessor-cycle check

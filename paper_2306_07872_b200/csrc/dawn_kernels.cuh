@@ -1,28 +1,34 @@
 // dawn_kernels.cuh — the persistent weighted-DAWN solver (GOVM + GSVM).
 //
-// One cooperative launch runs the whole round loop of the reference's
-// `while step < n` (solver.py:284, :356) on the device: no host sync per
-// round.  Each round r is two grid-synchronised phases:
+// One cooperative launch runs the reference's whole round loop
+// (`while step < n`, solver.py:284, :356) on the device with no host sync per
+// round.  Round r is two grid-synchronised phases:
 //
-//   S (snapshot/compact): frontier entries take a snapshot of their node's
-//      distance (snapshot-Jacobi semantics: every relax in round r reads the
-//      value as of the start of round r) and mark which frontier entry owns
-//      the first virtual edge of every TILE-edge tile.  GSVM builds its
-//      frontier here by compacting all finite rows (solver.py:287-289).
-//   X (expand): persistent CTAs claim TILE-edge tiles of the frontier's
-//      virtual edge list (merge-path style load balance, so hub rows of
-//      10^5 edges and 1-edge rows cost the same per edge), find each edge's
-//      row with a block max-scan over row-start marks, stream the packed
-//      (col, w) pairs, and relax with read-before-atomicMin on the ordered
-//      key.  The first lowering of a node in a round (write stamp) counts
-//      the write, the first discovery and the >=2-round nodes, and enqueues
-//      the node into the next frontier through a per-CTA buffer flushed with
-//      one packed 64-bit atomicAdd reserving (entries, edge offsets)
-//      together — the frontier "Copy beta to delta" of Alg. 2
-//       without an O(n) scan.
+//   S (frontier build): the frontier of round r — the nodes lowered in round
+//      r-1 (Alg. 2's "Copy beta to delta") or, for GSVM,
+//      every finite node (solver.py:287-289) — is laid out as entries
+//      {node, edge offset, row base, snapshot key}.  The snapshot key gives
+//      frontier-synchronous (snapshot-Jacobi) semantics: every relax of round
+//      r reads its row's distance as of the start of round r.  S also marks,
+//      for every TILE-edge tile of the frontier's virtual edge list, the entry
+//      owning the tile's first edge.  Two ways to build it:
+//        dense  — a coalesced sweep over all nodes selecting stamp == r-1
+//                 (after a heavy round; also counts that round's writes);
+//        sparse — snapshot of the queue the X phase filled (after a light round).
+//   X (expand): persistent CTAs stream the tiles (merge-path load balance:
+//      a hub row of 10^5 edges and a 1-edge row cost the same per edge), find
+//      each edge's row by a max-scan over row-start marks, stream the packed
+//      (col, w) pairs, and relax:
+//          cur = dist[v] (ld.cg, coherent at L2)
+//          cand < cur  =>  v WILL be lowered this round, so
+//          red.min(dist[v], cand) needs no return value, and the write stamp
+//          stamp[v] = r is a plain store (dense) or an atomic exchange whose
+//          old value elects the one thread that enqueues v (sparse).
+//      The reference's strict `>` (solver.py:298, :373) is `cand < cur` on the
+//      order-preserving key; the source guard (solver.py:299-303) flags.
 //
-// Optional passes: a predecessor pass (record_pred) and a predecessor-graph
-// cycle check by pointer doubling (integer weights with negative edges).
+// Optional passes: predecessors (record_pred) and the predecessor-graph
+// cycle check (integer weights with negative edges).
 #pragma once
 #include "dawn_device.cuh"
 
@@ -38,7 +44,8 @@ struct KParams {
   const uint32_t* ecol;                // SoA columns for 8-byte value types
   const unsigned long long* ew;        // SoA weights for 8-byte value types
   K* dist;
-  uint32_t* stamp;
+  uint32_t* stamp;                     // last round that lowered the node (0 = never)
+  uint8_t* wstate;                     // 0 never lowered, 1 lowered in one round, 2 in >= 2
   unsigned long long* pred;            // (round << 32) | ~u, or nullptr
   uint32_t* jmp0;
   uint32_t* jmp1;
@@ -54,6 +61,9 @@ struct KParams {
   int logn;                            // ceil(log2(n))
   int ebits;                           // packed reservation split
   unsigned max_rounds;
+  unsigned long long dense_edges;      // a round relaxing >= this many edges builds the next frontier densely
+  unsigned long long* prof;            // optional per-round timeline (4 words/round) or nullptr
+  unsigned prof_cap;                   // rounds the timeline can hold
 };
 
 template <class V, class EI>
@@ -69,13 +79,12 @@ struct __align__(16) Smem {
   unsigned long long scr64[NT / 32];
   uint32_t wmark[NT / 32];
   unsigned long long basepk;
-  uint32_t tile;
+  uint32_t tr[2][2];            // [parity][first row, last row] of the next tile
   int qcnt;
 };
 
 template <class V> struct EdgeAccess;
-// 4-byte value types: one 8-byte load per edge
-template <> struct EdgeAccess<int32_t> {
+template <> struct EdgeAccess<int32_t> {  // 4-byte value types: one 8-byte load per edge
   template <class P, class EI> __device__ __forceinline__ static void load(const P& p, EI pos, uint32_t& c, uint32_t& w) {
     uint2 x = ld_stream(p.e2 + pos); c = x.x; w = x.y;
   }
@@ -115,8 +124,18 @@ __device__ __forceinline__ void mark_tiles(uint32_t* tile_row, EI off, EI deg, u
   for (EI t = t0; t <= t1; ++t) tile_row[t] = entry;
 }
 
+// first-write bookkeeping of a node lowered in round r (runs exactly once per
+// (node, round)): first_discoveries (solver.py:378-379) and the nodes lowered
+// in >= 2 rounds (updated_ratio numerator, solver.py:258-262).
+__device__ __forceinline__ void count_write(uint8_t* wstate, uint32_t v, unsigned long long& acc_fd,
+                                            unsigned long long& acc_multi) {
+  const uint8_t ws = wstate[v];
+  if (ws == 0) { acc_fd++; wstate[v] = 1; }
+  else if (ws == 1) { acc_multi++; wstate[v] = 2; }
+}
+
 // ---------------------------------------------------------------------------
-// S phase, GOVM (and round 1 of GSVM): snapshot the frontier keys
+// S phase, sparse: snapshot the queue the previous X phase built
 // ---------------------------------------------------------------------------
 template <class V, class EI>
 __device__ void phase_snapshot(const KParams<V, EI>& P, int p) {
@@ -135,82 +154,174 @@ __device__ void phase_snapshot(const KParams<V, EI>& P, int p) {
 }
 
 // ---------------------------------------------------------------------------
-// S phase, GSVM rounds >= 2: every finite row with edges is rescanned
-// (solver.py:287-289); compaction builds the frontier with snapshots.
+// S phase, dense: one coalesced sweep over all nodes.  Counts round r-1's
+// writes (stamp == r-1) and selects GOVM's frontier (those nodes) or GSVM's
+// (every finite node, solver.py:287-289).  Each thread owns ITEMS consecutive
+// nodes and reads them with 128-bit loads; one packed block scan
+// (count << ebits | degree) places the chunk's entries.
 // ---------------------------------------------------------------------------
+template <class T>
+__device__ __forceinline__ void ldcg8(const T* p, T (&o)[ITEMS]) {
+  static_assert(ITEMS == 8, "vector loads assume 8 items");
+  if constexpr (sizeof(T) == 4) {
+    const uint4 a = __ldcg(reinterpret_cast<const uint4*>(p));
+    const uint4 b = __ldcg(reinterpret_cast<const uint4*>(p) + 1);
+    o[0] = (T)a.x; o[1] = (T)a.y; o[2] = (T)a.z; o[3] = (T)a.w;
+    o[4] = (T)b.x; o[5] = (T)b.y; o[6] = (T)b.z; o[7] = (T)b.w;
+  } else {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const ulonglong2 a = __ldcg(reinterpret_cast<const ulonglong2*>(p) + q);
+      o[2 * q] = (T)a.x; o[2 * q + 1] = (T)a.y;
+    }
+  }
+}
+template <class T>
+__device__ __forceinline__ void ldg8(const T* p, T (&o)[ITEMS]) {
+  if constexpr (sizeof(T) == 4) {
+    const uint4 a = __ldg(reinterpret_cast<const uint4*>(p));
+    const uint4 b = __ldg(reinterpret_cast<const uint4*>(p) + 1);
+    o[0] = (T)a.x; o[1] = (T)a.y; o[2] = (T)a.z; o[3] = (T)a.w;
+    o[4] = (T)b.x; o[5] = (T)b.y; o[6] = (T)b.z; o[7] = (T)b.w;
+  } else {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const ulonglong2 a = __ldg(reinterpret_cast<const ulonglong2*>(p) + q);
+      o[2 * q] = (T)a.x; o[2 * q + 1] = (T)a.y;
+    }
+  }
+}
+
 template <class V, class EI>
-__device__ void phase_compact_all(const KParams<V, EI>& P, int p, Smem<V, EI>& s) {
+__device__ void phase_compact(const KParams<V, EI>& P, int p, uint32_t r, Smem<V, EI>& s,
+                              unsigned long long& acc_w, unsigned long long& acc_fd,
+                              unsigned long long& acc_multi, uint32_t& prev_w) {
   using VT = Val<V>;
   using K = typename VT::K;
   const uint32_t n = P.n;
   const uint32_t nchunks = (n + TILE - 1) / TILE;
+  const bool gsvm = P.algo == 1;
+  const int eb = P.ebits;
+  // stamps of the thread's next chunk are prefetched one iteration ahead
+  uint32_t nst[ITEMS];
+  auto load_stamps = [&](uint32_t c, uint32_t (&o)[ITEMS]) {
+    const uint32_t u = c * TILE + threadIdx.x * ITEMS;
+    if (u + ITEMS <= n) {
+      ldcg8<uint32_t>(P.stamp + u, o);
+    } else {
+#pragma unroll
+      for (int j = 0; j < ITEMS; ++j) o[j] = (u + j < n) ? ldcg(P.stamp + u + j) : 0u;
+    }
+  };
+  if (blockIdx.x < nchunks) load_stamps(blockIdx.x, nst);
   for (uint32_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
-    uint32_t u0 = c * TILE + threadIdx.x * ITEMS;
-    uint32_t selmask = 0;
-    EI degs[ITEMS];
-    EI rs[ITEMS];
+    const uint32_t u0 = c * TILE + threadIdx.x * ITEMS;
+    uint32_t stv[ITEMS];
+#pragma unroll
+    for (int j = 0; j < ITEMS; ++j) stv[j] = nst[j];
+    if (c + gridDim.x < nchunks) load_stamps(c + gridDim.x, nst);
     K keys[ITEMS];
+    EI rp[ITEMS + 1];
+    const bool full = u0 + ITEMS <= n;
+    unsigned wm = 0;  // lowered in round r-1
+#pragma unroll
+    for (int j = 0; j < ITEMS; ++j) wm |= (unsigned)(stv[j] == r - 1 && u0 + j < n) << j;
+    const unsigned want = gsvm ? ((u0 < n) ? 0xFFu : 0u) : wm;
+    // keys, row bounds and write states: one batch of vector loads
+    unsigned sel = 0;
     uint32_t mycnt = 0;
     EI mydeg = 0;
+    uint2 ws = make_uint2(0, 0);
+    if (wm) {
+      if (full) ws = __ldcg(reinterpret_cast<const uint2*>(P.wstate + u0));
+      else {
+        uint8_t* b = reinterpret_cast<uint8_t*>(&ws);
 #pragma unroll
-    for (int j = 0; j < ITEMS; ++j) {
-      uint32_t u = u0 + j;
-      degs[j] = 0;
-      rs[j] = 0;
-      keys[j] = VT::INF;
-      if (u < n) {
-        K k = ldcg(P.dist + u);
-        keys[j] = k;
-        if (k != VT::INF) {
-          EI a = __ldg(P.row_ptr + u), b = __ldg(P.row_ptr + u + 1);
-          if (b > a) {
-            selmask |= 1u << j;
-            degs[j] = b - a;
-            rs[j] = a;
-            mycnt++;
-            mydeg += b - a;
-          }
-        }
+        for (int j = 0; j < ITEMS; ++j) b[j] = (u0 + j < n) ? ldcg(P.wstate + u0 + j) : (uint8_t)0;
       }
     }
-    EI tot_deg;
-    EI incl_deg = block_incl_sum<EI>(mydeg, s.scr, &tot_deg);
-    unsigned long long tot_cnt;
-    unsigned long long incl_cnt = block_incl_sum<unsigned long long>(mycnt, s.scr64, &tot_cnt);
-    if (threadIdx.x == 0 && tot_cnt > 0) {
-      s.basepk = atomicAdd(&P.st->res[p], (tot_cnt << P.ebits) | (unsigned long long)tot_deg);
-    }
-    __syncthreads();
-    if (tot_cnt > 0) {
-      const unsigned long long bp = s.basepk;
-      uint32_t pos = (uint32_t)(pk_count(bp, P.ebits) + incl_cnt - mycnt);
-      EI off = (EI)pk_edges(bp, P.ebits) + incl_deg - mydeg;
+    if (want) {
+      if (full) {
+        ldcg8<K>(P.dist + u0, keys);
+        ldg8<EI>(P.row_ptr + u0, *reinterpret_cast<EI(*)[ITEMS]>(rp));
+        rp[ITEMS] = __ldg(P.row_ptr + u0 + ITEMS);
+      } else {
+#pragma unroll
+        for (int j = 0; j < ITEMS; ++j) {
+          keys[j] = (u0 + j < n) ? ldcg(P.dist + u0 + j) : VT::INF;
+          rp[j] = (u0 + j <= n) ? __ldg(P.row_ptr + u0 + j) : (EI)0;
+        }
+        rp[ITEMS] = (u0 + ITEMS <= n) ? __ldg(P.row_ptr + u0 + ITEMS) : (EI)0;
+      }
 #pragma unroll
       for (int j = 0; j < ITEMS; ++j) {
-        if (selmask & (1u << j)) {
-          P.qnode[p][pos] = u0 + j;
-          P.qoff[p][pos] = off;
-          P.qbase[p][pos] = rs[j] - off;
-          P.qkey[p][pos] = keys[j];
-          mark_tiles<EI>(P.tile_row, off, degs[j], pos);
-          pos++;
-          off += degs[j];
+        if (((want >> j) & 1u) && u0 + j < n && keys[j] != VT::INF && rp[j + 1] > rp[j]) {
+          sel |= 1u << j;
+          mycnt++;
+          mydeg += rp[j + 1] - rp[j];
         }
       }
     }
+    // write bookkeeping for round r-1 (first_discoveries, >= 2-round nodes)
+    if (wm) {
+      uint8_t* b = reinterpret_cast<uint8_t*>(&ws);
+#pragma unroll
+      for (int j = 0; j < ITEMS; ++j) {
+        if ((wm >> j) & 1u) {
+          prev_w++;
+          acc_w++;
+          if (b[j] == 0) { acc_fd++; b[j] = 1; }
+          else if (b[j] == 1) { acc_multi++; b[j] = 2; }
+        }
+      }
+      if (full) *reinterpret_cast<uint2*>(P.wstate + u0) = ws;
+      else {
+#pragma unroll
+        for (int j = 0; j < ITEMS; ++j)
+          if (u0 + j < n) P.wstate[u0 + j] = b[j];
+      }
+    }
+    // 4. place the chunk's entries: one packed scan, one reservation
+    const unsigned long long mine = ((unsigned long long)mycnt << eb) | (unsigned long long)mydeg;
+    unsigned long long tot;
+    const unsigned long long incl = block_incl_sum<unsigned long long>(mine, s.scr64, &tot);
+    if (threadIdx.x == 0 && tot != 0ull) s.basepk = atomicAdd(&P.st->res[p], tot);
     __syncthreads();
+    if (sel) {
+      const unsigned long long at = s.basepk + incl - mine;
+      uint32_t pos = (uint32_t)pk_count(at, eb);
+      EI off = (EI)pk_edges(at, eb);
+#pragma unroll
+      for (int j = 0; j < ITEMS; ++j) {
+        if (sel & (1u << j)) {
+          const EI deg = rp[j + 1] - rp[j];
+          P.qnode[p][pos] = u0 + j;
+          P.qoff[p][pos] = off;
+          P.qbase[p][pos] = rp[j] - off;
+          P.qkey[p][pos] = keys[j];
+          mark_tiles<EI>(P.tile_row, off, deg, pos);
+          pos++;
+          off += deg;
+        }
+      }
+    }
   }
 }
 
 // ---------------------------------------------------------------------------
 // X phase: tiles of the frontier's virtual edge list.
-//   PRED == false : relax + count + enqueue (GOVM)
+//   PRED == false : relax (+ enqueue when !dense)
 //   PRED == true  : predecessor pass — among this round's frontier edges that
 //                   reproduce the final value of a node lowered this round,
 //                   keep the smallest source node (deterministic witness).
+// Static tile assignment t = blockIdx.x + k*G (every tile has TILE edges).
+// Software pipeline: while tile t streams, the row metadata of tile t+G and
+// the row range of tile t+2G are already in flight (registers).
 // ---------------------------------------------------------------------------
+constexpr uint32_t SENT = 0xFFFFFFFFu;
+
 template <class V, class EI, bool PRED>
-__device__ void phase_expand(const KParams<V, EI>& P, int p, uint32_t r, Smem<V, EI>& s,
+__device__ void phase_expand(const KParams<V, EI>& P, int p, uint32_t r, bool dense, Smem<V, EI>& s,
                              unsigned long long& acc_w, unsigned long long& acc_fd,
                              unsigned long long& acc_multi, uint32_t& round_w) {
   using VT = Val<V>;
@@ -221,40 +332,88 @@ __device__ void phase_expand(const KParams<V, EI>& P, int p, uint32_t r, Smem<V,
   const EI E = (EI)pk_edges(pk, P.ebits);
   if (E == 0) return;
   const EI T = (E + (EI)(TILE - 1)) / (EI)TILE;
+  const EI G = gridDim.x;
+  EI t = blockIdx.x;
+  if (t >= T) return;
   const int np = p ^ 1;
-  const bool govm = (P.algo == 0);
   const uint32_t src = P.src;
-  unsigned* tctr = PRED ? &P.st->tile_ctr2[p] : &P.st->tile_ctr[p];
   const int tid = threadIdx.x;
+  const uint32_t* tile_row = P.tile_row;
+  const EI* qbase = P.qbase[p];
+  const EI* qoff = P.qoff[p];
+  const K* qkey = P.qkey[p];
+  const uint32_t* qnode = P.qnode[p];
+  // rows of tile q are [tile_row[q], tile_row[q+1]] (the last tile ends at cnt-1)
+  auto row_bound = [&](EI q, int which) -> uint32_t {
+    const EI x = q + (EI)which;
+    return (x < T) ? ldcg(tile_row + x) : cnt - 1;
+  };
 
-  for (;;) {
-    if (tid == 0) s.tile = atomicAdd(tctr, 1u);
-    __syncthreads();
-    const EI t = (EI)s.tile;
-    if (t >= T) break;
+  // prologue: rows of tile t into registers, row range of tile t+G
+  uint32_t cur_i0 = row_bound(t, 0), cur_il = row_bound(t, 1);
+  uint32_t tr_nx = 0;  // tid 0 / 1: first / last row of the tile after the current one
+  if (tid < 2 && t + G < T) tr_nx = row_bound(t + G, tid);
+  EI pf_base = 0, pf_off = 0;
+  K pf_key = 0;
+  uint32_t pf_node = 0;
+  if ((uint32_t)tid <= cur_il - cur_i0) {
+    const uint32_t i = cur_i0 + tid;
+    pf_base = ldcg(qbase + i);
+    pf_off = ldcg(qoff + i);
+    pf_key = ldcg(qkey + i);
+    if (PRED) pf_node = ldcg(qnode + i);
+  }
+  int par = 0;
+
+  for (; t < T; t += G) {
     const EI e0 = t * (EI)TILE;
     const EI e1 = (E - e0 < (EI)TILE) ? E : e0 + (EI)TILE;
-    const uint32_t i0 = ldcg(P.tile_row + t);
-    const uint32_t ilast = (t + 1 < T) ? ldcg(P.tile_row + t + 1) : cnt - 1;
+    const uint32_t i0 = cur_i0, ilast = cur_il;
     const uint32_t nrows = ilast - i0 + 1;
     const bool multi_row = nrows > 1;
-    if (multi_row) reinterpret_cast<uint4*>(s.mark)[tid] = make_uint4(0, 0, 0, 0);
+    // ---- publish this tile's (prefetched) rows and the next tile's range ----
+    reinterpret_cast<uint4*>(s.mark)[tid] = make_uint4(0, 0, 0, 0);
+    if ((uint32_t)tid < nrows) {
+      s.base[tid] = pf_base;
+      s.key[tid] = pf_key;
+      if (PRED) s.qnode[tid] = pf_node;
+    }
+    if (tid < 2) s.tr[par][tid] = tr_nx;
     __syncthreads();
-    for (uint32_t k = tid; k < nrows; k += NT) {
-      const uint32_t i = i0 + k;
-      s.base[k] = ldcg(P.qbase[p] + i);
-      s.key[k] = ldcg(P.qkey[p] + i);
-      if (PRED) s.qnode[k] = ldcg(P.qnode[p] + i);
-      if (multi_row) {
-        EI off = ldcg(P.qoff[p] + i);
-        EI start = off > e0 ? off : e0;
+    if (multi_row) {  // row-start marks (after the zeroing above is complete)
+      if ((uint32_t)tid < nrows) {
+        const EI start = pf_off > e0 ? pf_off : e0;
+        if (start < e1) s.mark[start - e0] = (uint16_t)tid;
+      }
+      for (uint32_t k = NT + tid; k < nrows; k += NT) {  // rows beyond the first NT (tiny rows)
+        const uint32_t i = i0 + k;
+        s.base[k] = ldcg(qbase + i);
+        s.key[k] = ldcg(qkey + i);
+        if (PRED) s.qnode[k] = ldcg(qnode + i);
+        const EI off = ldcg(qoff + i);
+        const EI start = off > e0 ? off : e0;
         if (start < e1) s.mark[start - e0] = (uint16_t)k;
       }
     }
-    __syncthreads();
+    // ---- advance the pipeline: rows of tile t+G, range of tile t+2G ----
+    const EI tn = t + G;
+    if (tn < T) {
+      cur_i0 = s.tr[par][0];
+      cur_il = s.tr[par][1];
+      if ((uint32_t)tid <= cur_il - cur_i0) {
+        const uint32_t i = cur_i0 + tid;
+        pf_base = ldcg(qbase + i);
+        pf_off = ldcg(qoff + i);
+        pf_key = ldcg(qkey + i);
+        if (PRED) pf_node = ldcg(qnode + i);
+      }
+      if (tid < 2 && tn + G < T) tr_nx = row_bound(tn + G, tid);
+    }
+    par ^= 1;
+    if (multi_row) __syncthreads();
     if (multi_row) {
       // inclusive max-scan of the marks: each thread owns ITEMS consecutive slots
-      uint4 mv = reinterpret_cast<uint4*>(s.mark)[tid];
+      const uint4 mv = reinterpret_cast<uint4*>(s.mark)[tid];
       uint32_t m8[8] = {mv.x & 0xFFFFu, mv.x >> 16, mv.y & 0xFFFFu, mv.y >> 16,
                         mv.z & 0xFFFFu, mv.z >> 16, mv.w & 0xFFFFu, mv.w >> 16};
       uint32_t run = 0;
@@ -264,83 +423,114 @@ __device__ void phase_expand(const KParams<V, EI>& P, int p, uint32_t r, Smem<V,
       uint32_t incl = run;
 #pragma unroll
       for (int d = 1; d < 32; d <<= 1) {
-        uint32_t y = __shfl_up_sync(0xffffffffu, incl, d);
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, d);
         if (lane >= d) incl = max(incl, y);
       }
       uint32_t excl = __shfl_up_sync(0xffffffffu, incl, 1);
       if (lane == 0) excl = 0;
       if (lane == 31) s.wmark[warp] = incl;
       __syncthreads();
-      uint32_t pre = excl;
-      for (int w = 0; w < warp; ++w) pre = max(pre, s.wmark[w]);
+      uint32_t pre_w = excl;
+      for (int w = 0; w < warp; ++w) pre_w = max(pre_w, s.wmark[w]);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) m8[j] = max(m8[j], pre);
+      for (int j = 0; j < 8; ++j) m8[j] = max(m8[j], pre_w);
       reinterpret_cast<uint4*>(s.mark)[tid] =
           make_uint4(m8[0] | (m8[1] << 16), m8[2] | (m8[3] << 16), m8[4] | (m8[5] << 16),
                      m8[6] | (m8[7] << 16));
       __syncthreads();
     }
 
-    // ---- stream the tile's edges: ITEMS independent loads per thread ----
+    // ---- phase 1: positions, then all edge loads back to back ----
     uint32_t col[ITEMS];
-    K cand[ITEMS];
+    WB wv[ITEMS];
     uint32_t rowk[ITEMS];
-#pragma unroll
-    for (int j = 0; j < ITEMS; ++j) {
-      const uint32_t idx = j * NT + tid;
-      const EI e = e0 + idx;
-      col[j] = 0xFFFFFFFFu;
-      rowk[j] = 0;
-      if (e < e1) {
-        const uint32_t k = multi_row ? (uint32_t)s.mark[idx] : 0u;
-        rowk[j] = k;
-        WB w;
-        EdgeAccess<V>::load(P, s.base[k] + e, col[j], w);
-        cand[j] = VT::relax(s.key[k], w);
-        if (!VT::usable(cand[j])) col[j] = 0xFFFFFFFFu;
-      }
-    }
-    if (!PRED) {
-      K cur[ITEMS];
-#pragma unroll
-      for (int j = 0; j < ITEMS; ++j) cur[j] = (col[j] != 0xFFFFFFFFu) ? P.dist[col[j]] : (K)0;
+    unsigned okm = 0;
+    {
+      EI pos[ITEMS];
+      const EI safe = s.base[0] + e0;  // first edge of the tile: always a valid address
 #pragma unroll
       for (int j = 0; j < ITEMS; ++j) {
-        const uint32_t v = col[j];
-        if (v == 0xFFFFFFFFu || !(cand[j] < cur[j])) continue;
-        if (v == src) {  // source guard (solver.py:299-303, :374-376, seed :236-239)
-          P.st->flag = 1u;
-          continue;
+        const uint32_t idx = j * NT + tid;
+        const EI e = e0 + idx;
+        const bool ok = e < e1;
+        okm |= (unsigned)ok << j;
+        const uint32_t k = (multi_row && ok) ? (uint32_t)s.mark[idx] : 0u;
+        rowk[j] = k;
+        pos[j] = ok ? s.base[k] + e : safe;
+      }
+#pragma unroll
+      for (int j = 0; j < ITEMS; ++j) EdgeAccess<V>::load(P, pos[j], col[j], wv[j]);
+    }
+    // ---- phase 2: candidates ----
+    K cand[ITEMS];
+#pragma unroll
+    for (int j = 0; j < ITEMS; ++j) {
+      cand[j] = VT::relax(s.key[rowk[j]], wv[j]);
+      if (!((okm >> j) & 1u) || !VT::usable(cand[j])) col[j] = SENT;
+    }
+    if (!PRED) {
+      // ---- phase 3: coherent read-before-write filter, all gathers in flight ----
+      K cur[ITEMS];
+#pragma unroll
+      for (int j = 0; j < ITEMS; ++j) cur[j] = (col[j] != SENT) ? ldcg(P.dist + col[j]) : (K)0;
+      unsigned need = 0;
+#pragma unroll
+      for (int j = 0; j < ITEMS; ++j) {
+        if (col[j] != SENT && cand[j] < cur[j]) {
+          if (col[j] == src) P.st->flag = 1u;  // source guard (solver.py:299-303, :374-376, :236-239)
+          else need |= 1u << j;
         }
-        const K old = atomicMin(P.dist + v, cand[j]);
-        if (!(cand[j] < old)) continue;
-        const unsigned os = atomicMax(P.stamp + v, r << 1);
-        if ((os >> 1) >= r) continue;  // already lowered earlier in this round
-        round_w++;
-        acc_w++;
-        if (os == 0u) {
-          acc_fd++;  // left infinity (first_discoveries, solver.py:378-379)
-        } else {
-          if (!(os & 1u)) acc_multi++;  // second round that lowers v
-          atomicOr(P.stamp + v, 1u);
+      }
+      // ---- phase 4: fire-and-forget min (cand < cur proves v is lowered this round) ----
+#pragma unroll
+      for (int j = 0; j < ITEMS; ++j)
+        if ((need >> j) & 1u) atomicMin(P.dist + col[j], cand[j]);
+      if (dense) {
+#pragma unroll
+        for (int j = 0; j < ITEMS; ++j)
+          if ((need >> j) & 1u) P.stamp[col[j]] = r;
+      } else if (need) {
+        unsigned os[ITEMS];
+#pragma unroll
+        for (int j = 0; j < ITEMS; ++j)
+          if ((need >> j) & 1u) os[j] = atomicExch(P.stamp + col[j], r);
+        unsigned first = 0;
+#pragma unroll
+        for (int j = 0; j < ITEMS; ++j) {
+          if (((need >> j) & 1u) && os[j] != r) {  // the one thread electing v this round
+            first |= 1u << j;
+            round_w++;
+            acc_w++;
+            count_write(P.wstate, col[j], acc_fd, acc_multi);
+          }
         }
-        if (govm) {
-          const EI a = __ldg(P.row_ptr + v), b = __ldg(P.row_ptr + v + 1);
-          if (b > a) {  // rows without edges never need a rescan
-            const int slot = atomicAdd(&s.qcnt, 1);
-            s.qnode[slot] = v;
-            s.qrs[slot] = a;
-            s.qdeg[slot] = b - a;
+        if (first) {
+          EI a[ITEMS], b[ITEMS];
+#pragma unroll
+          for (int j = 0; j < ITEMS; ++j) {
+            if ((first >> j) & 1u) {
+              a[j] = __ldg(P.row_ptr + col[j]);
+              b[j] = __ldg(P.row_ptr + col[j] + 1);
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < ITEMS; ++j) {
+            if (((first >> j) & 1u) && b[j] > a[j]) {  // rows without edges never need a rescan
+              const int slot = atomicAdd(&s.qcnt, 1);
+              s.qnode[slot] = col[j];
+              s.qrs[slot] = a[j];
+              s.qdeg[slot] = b[j] - a[j];
+            }
           }
         }
       }
-      if (govm) {
+      if (!dense) {
         // ---- flush the enqueue buffer: one packed reservation per tile ----
         __syncthreads();
         const int q = s.qcnt;
         if (q > 0) {
           EI carry = 0;
-          for (int c0 = 0; c0 < q; c0 += NT) {
+          for (int c0 = 0; c0 < q; c0 += NT) {  // exclusive degree scan -> local offsets
             const int i = c0 + tid;
             const EI d = (i < q) ? s.qdeg[i] : (EI)0;
             EI tot;
@@ -351,6 +541,7 @@ __device__ void phase_expand(const KParams<V, EI>& P, int p, uint32_t r, Smem<V,
           if (tid == 0) {
             s.basepk = atomicAdd(&P.st->res[np],
                                  ((unsigned long long)q << P.ebits) | (unsigned long long)carry);
+            s.qcnt = 0;
           }
           __syncthreads();
           const unsigned long long bp = s.basepk;
@@ -362,24 +553,25 @@ __device__ void phase_expand(const KParams<V, EI>& P, int p, uint32_t r, Smem<V,
             P.qoff[np][bc + i] = off;
             P.qbase[np][bc + i] = s.qrs[i] - off;
           }
-          __syncthreads();
-          if (tid == 0) s.qcnt = 0;
         }
       }
     } else {
+      unsigned sv[ITEMS];
+#pragma unroll
+      for (int j = 0; j < ITEMS; ++j)
+        sv[j] = (col[j] != SENT && col[j] != src) ? ldcg(P.stamp + col[j]) : 0u;
+      K dv[ITEMS];
+#pragma unroll
+      for (int j = 0; j < ITEMS; ++j) dv[j] = (sv[j] == r) ? ldcg(P.dist + col[j]) : (K)0;
 #pragma unroll
       for (int j = 0; j < ITEMS; ++j) {
-        const uint32_t v = col[j];
-        if (v == 0xFFFFFFFFu || v == src) continue;
-        const unsigned sv = ldcg(P.stamp + v);
-        if ((sv >> 1) != r) continue;
-        if (cand[j] == ldcg(P.dist + v)) {
+        if (sv[j] == r && col[j] != SENT && col[j] != src && cand[j] == dv[j]) {
           const uint32_t u = s.qnode[rowk[j]];
-          atomicMax(P.pred + v, ((unsigned long long)r << 32) | (unsigned long long)(~u));
+          atomicMax(P.pred + col[j], ((unsigned long long)r << 32) | (unsigned long long)(~u));
         }
       }
     }
-    __syncthreads();
+    __syncthreads();  // everyone is done with marks / rows / the enqueue buffer
   }
 }
 
@@ -424,8 +616,10 @@ __device__ bool pred_graph_has_cycle(const KParams<V, EI>& P) {
 // ---------------------------------------------------------------------------
 // the persistent kernel
 // ---------------------------------------------------------------------------
-template <class V, class EI>
-__global__ void __launch_bounds__(NT) dawn_persistent(KParams<V, EI> P) {
+// WITH_PRED instantiates the predecessor pass and the negative-cycle check;
+// the plain instance carries none of their registers.
+template <class V, class EI, bool WITH_PRED>
+__global__ void __launch_bounds__(NT, DAWN_MIN_BLOCKS) dawn_persistent(KParams<V, EI> P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem<V, EI>& s = *reinterpret_cast<Smem<V, EI>*>(smem_raw);
   DevState* st = P.st;
@@ -434,66 +628,90 @@ __global__ void __launch_bounds__(NT) dawn_persistent(KParams<V, EI> P) {
   __syncthreads();
 
   uint32_t r = ldcg(&st->round);
+  bool dense_prev = ldcg(&st->dense_prev) != 0u;  // how round r-1 recorded its writes
+  bool skip_s = ldcg(&st->resume_x) != 0u;         // stepping: round r's frontier is already built
   unsigned long long acc_w = 0, acc_fd = 0, acc_multi = 0, acc_r = 0;
   unsigned rounds = 0;
   for (;;) {
     const int p = r & 1;
-    // ---- termination (solver.py:284-285, :313-317, :356-358, :388-395) ----
-    if (r >= 2) {
-      const unsigned long long wprev = ldcg(&st->wround[(r - 1) & 1]);
-      bool stop = false, capflag = false;
-      if (r - 1 >= 2 && wprev == 0) stop = true;        // a loop round wrote nothing
-      else if (r - 1 >= P.n) { stop = true; capflag = wprev > 0; }  // cap reached still writing
-      if (stop) {
-        if (leader) {
-          st->steps = r - 1;
-          if (capflag) st->flag = 1u;
-          st->done = 1u;
-          st->round = r;
-        }
-        break;
+    const bool prof = leader && P.prof != nullptr && r < P.prof_cap;
+    if (!skip_s) {
+      if (prof) P.prof[4 * r + 0] = globaltimer();
+      // ---- S phase: build round r's frontier ----
+      if (leader) {
+        st->res[p ^ 1] = 0ull;  // queue of round r+1 (filled by X_r or S_{r+1})
+        st->wround[p] = 0ull;   // writes of round r (counted in X_r or S_{r+1})
       }
-      if (P.negcheck_period > 0 && r > 2 && ((r - 1) % (unsigned)P.negcheck_period) == 0) {
-        if (pred_graph_has_cycle(P)) {
+      if (r >= 2 && (dense_prev || P.algo == 1)) {
+        uint32_t prev_w = 0;
+        phase_compact<V, EI>(P, p, r, s, acc_w, acc_fd, acc_multi, prev_w);
+        prev_w = __reduce_add_sync(0xffffffffu, prev_w);
+        if ((threadIdx.x & 31) == 0 && prev_w) atomicAdd(&st->wround[p ^ 1], (unsigned long long)prev_w);
+      } else {
+        phase_snapshot<V, EI>(P, p);
+      }
+      grid_sync(&st->bar);
+      // ---- termination (solver.py:284-285, :313-317, :356-358, :388-395) ----
+      if (r >= 2) {
+        const unsigned long long wprev = ldcg(&st->wround[p ^ 1]);
+        bool stop = false, capflag = false;
+        if (r - 1 >= 2 && wprev == 0) stop = true;                   // a loop round wrote nothing
+        else if (r - 1 >= P.n) { stop = true; capflag = wprev > 0; }  // cap reached still writing
+        if (stop) {
           if (leader) {
             st->steps = r - 1;
-            st->flag = 1u;
-            st->early = 1u;
+            if (capflag) st->flag = 1u;
             st->done = 1u;
             st->round = r;
           }
           break;
         }
+        if (WITH_PRED && P.negcheck_period > 0 && r > 2 && ((r - 1) % (unsigned)P.negcheck_period) == 0) {
+          if (pred_graph_has_cycle(P)) {
+            if (leader) {
+              st->steps = r - 1;
+              st->flag = 1u;
+              st->early = 1u;
+              st->done = 1u;
+              st->round = r;
+            }
+            break;
+          }
+        }
+      }
+      if (rounds == P.max_rounds) {  // stepping: resume at X_r next launch
+        if (leader) {
+          st->round = r;
+          st->resume_x = 1u;
+        }
+        break;
       }
     }
-    if (rounds == P.max_rounds) {
-      if (leader) st->round = r;
-      break;
-    }
-    // ---- S phase ----
-    if (leader) {
-      st->res[p ^ 1] = 0ull;
-      st->wround[p] = 0ull;
-      st->tile_ctr[p] = 0u;
-      st->tile_ctr2[p] = 0u;
-    }
-    if (P.algo == 1 && r >= 2) phase_compact_all<V, EI>(P, p, s);
-    else phase_snapshot<V, EI>(P, p);
-    grid_sync(&st->bar);
+    skip_s = false;
     // ---- X phase ----
-    if (leader) acc_r += pk_edges(ldcg(&st->res[p]), P.ebits);  // relaxations (solver.py:297, :372)
+    const unsigned long long E = pk_edges(ldcg(&st->res[p]), P.ebits);
+    const bool dense = P.algo == 1 || E >= P.dense_edges;
+    if (leader) acc_r += E;  // relaxations (solver.py:297, :372)
+    if (prof) {
+      P.prof[4 * r + 1] = globaltimer();
+      P.prof[4 * r + 3] = ldcg(&st->res[p]);
+    }
     uint32_t round_w = 0;
-    phase_expand<V, EI, false>(P, p, r, s, acc_w, acc_fd, acc_multi, round_w);
+    phase_expand<V, EI, false>(P, p, r, dense, s, acc_w, acc_fd, acc_multi, round_w);
     round_w = __reduce_add_sync(0xffffffffu, round_w);
     if ((threadIdx.x & 31) == 0 && round_w) atomicAdd(&st->wround[p], (unsigned long long)round_w);
     grid_sync(&st->bar);
-    if (P.pred_on) {
-      phase_expand<V, EI, true>(P, p, r, s, acc_w, acc_fd, acc_multi, round_w);
+    if (leader) st->resume_x = 0u;  // every CTA has read it (first barrier passed)
+    if constexpr (WITH_PRED) {
+      phase_expand<V, EI, true>(P, p, r, dense, s, acc_w, acc_fd, acc_multi, round_w);
       grid_sync(&st->bar);
     }
+    if (prof) P.prof[4 * r + 2] = globaltimer();
+    dense_prev = dense;
     ++r;
     ++rounds;
   }
+  if (leader) st->dense_prev = dense_prev ? 1u : 0u;
   // flush per-thread counters
   acc_w = warp_sum_u64(acc_w);
   acc_fd = warp_sum_u64(acc_fd);
@@ -525,9 +743,9 @@ __global__ void dawn_init_solve(KParams<V, EI> P) {
     P.qoff[1][0] = 0;
     P.qbase[1][0] = a;
     st->wround[0] = st->wround[1] = 0ull;
-    st->tile_ctr[0] = st->tile_ctr[1] = 0u;
-    st->tile_ctr2[0] = st->tile_ctr2[1] = 0u;
     st->round = 1u;
+    st->dense_prev = 0u;
+    st->resume_x = 0u;
     st->done = 0u;
     st->flag = 0u;
     st->early = 0u;

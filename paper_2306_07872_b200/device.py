@@ -23,6 +23,24 @@ _cache: "weakref.WeakKeyDictionary[object, dict]" = weakref.WeakKeyDictionary()
 _strong_cache: dict[int, tuple[object, dict]] = {}
 
 _default_precision = "auto"
+_tuning: dict[str, float] = {}
+
+
+def set_tuning(**knobs: float) -> None:
+    """Process-wide solver tuning (``dawn_solver_tune``); results never depend on it.
+
+    ``dense_edges_per_node``: rounds relaxing >= value * n edges rebuild the
+    next frontier by a coalesced sweep instead of an enqueue (default 0.5).
+    Applies to solvers created afterwards and to existing cached ones.
+    """
+    _tuning.update({k: float(v) for k, v in knobs.items()})
+    with _cache_lock:
+        for per in list(_cache.values()):
+            for dg in per.values():
+                dg.retune()
+        for _, per in _strong_cache.values():
+            for dg in per.values():
+                dg.retune()
 
 
 def set_default_precision(precision: str) -> None:
@@ -104,14 +122,24 @@ class DeviceGraph:
 
     # -- solvers ------------------------------------------------------------
     def solver(self, flags: int = 0) -> int:
-        key = flags & (N.F_PRED | N.F_NEGCHECK)
+        key = flags & (N.F_PRED | N.F_NEGCHECK | N.F_PROFILE)
         with self.lock:
             s = self._solvers.get(key)
             if s is None:
                 h = c_void_p()
                 N.check(N.lib().dawn_solver_create(self.handle, key, byref(h)))
                 s = self._solvers[key] = h.value
+                self._apply_tuning(s)
             return s
+
+    def _apply_tuning(self, s: int) -> None:
+        for k, v in _tuning.items():
+            N.check(N.lib().dawn_solver_tune(s, k.encode(), v))
+
+    def retune(self) -> None:
+        with self.lock:
+            for s in self._solvers.values():
+                self._apply_tuning(s)
 
     def device_bytes(self) -> int:
         b = c_int64(0)

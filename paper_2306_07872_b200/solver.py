@@ -272,7 +272,7 @@ def _solve_traced(g, source: int, algo: int, record_pred: bool, trace, precision
         N.check(L.dawn_sssp_begin(s, int(source), algo, flags, stream))
         N.check(L.dawn_sssp_advance(s, 1, byref(rnd), byref(done), stream))  # seeding round
         N.check(L.dawn_solver_state(s, None, stamp.ctypes.data, stream))
-        prev_written = np.flatnonzero((stamp >> 1) == 1).tolist()
+        prev_written = np.flatnonzero(stamp == 1).tolist()
         last = rnd.value
         while True:
             N.check(L.dawn_sssp_advance(s, 1, byref(rnd), byref(done), stream))
@@ -280,7 +280,7 @@ def _solve_traced(g, source: int, algo: int, record_pred: bool, trace, precision
                 break
             last = rnd.value
             N.check(L.dawn_solver_state(s, dist.ctypes.data, stamp.ctypes.data, stream))
-            written = np.flatnonzero((stamp >> 1) == last).tolist()
+            written = np.flatnonzero(stamp == last).tolist()
             trace(int(last), prev_written, written, dist.tolist())
             prev_written = written
         dist_out = np.empty(n, dtype=np.float64)
@@ -339,7 +339,7 @@ def seed_source(g, source: int, alpha: list, delta: list, stats: SolveStats | No
         N.check(L.dawn_solver_state(s, dist.ctypes.data, stamp.ctypes.data, stream))
         st = N.Stats()
         N.check(L.dawn_solver_result(s, None, None, byref(st), stream))
-    written = np.flatnonzero((stamp >> 1) == 1).tolist()
+    written = np.flatnonzero(stamp == 1).tolist()
     for j in written:
         was_inf = alpha[j] == inf
         alpha[j] = float(dist[j])

@@ -81,7 +81,7 @@ def test_fp32_path(gpu, name):
 # ---------------------------------------------------------------------------
 # reference test-suite behaviours (pkg/tests/test_solver.py), on the device
 # ---------------------------------------------------------------------------
-def test_seed_source(gpu):
+def test_seed_source(gpu, frontier_mode):
     g = make_csr(2, [(0, 1, 2.0), (0, 1, 1.0)])
     alpha, delta = [0.0, inf], [False, False]
     P.seed_source(g, 0, alpha, delta)
@@ -152,7 +152,7 @@ def test_predecessors(gpu):
                 assert math.isclose(total, dv.dist[j], rel_tol=0.0, abs_tol=1e-9)
 
 
-def test_trace_frontier_soundness(gpu):
+def test_trace_frontier_soundness(gpu, frontier_mode):
     for name in golden_names("rnd_uniform02_")[:8]:
         g = golden_graph(name)
         records = []
@@ -215,8 +215,16 @@ def test_determinism_and_stream_reuse(gpu):
 # ---------------------------------------------------------------------------
 # randomized parity against the oracle, all value types
 # ---------------------------------------------------------------------------
+@pytest.fixture(params=[0.5, 0.0, 1e9], ids=["auto", "all-dense", "all-sparse"])
+def frontier_mode(request):
+    """Run under the default dense/sparse frontier policy and both extremes."""
+    P.set_tuning(dense_edges_per_node=request.param)
+    yield request.param
+    P.set_tuning(dense_edges_per_node=0.5)
+
+
 @pytest.mark.parametrize("seed", range(24))
-def test_random_graphs_vs_oracle(gpu, seed):
+def test_random_graphs_vs_oracle(gpu, seed, frontier_mode):
     rng = np.random.default_rng(seed)
     n = int(rng.integers(2, 400))
     m = int(rng.integers(0, 6 * n))
@@ -252,7 +260,7 @@ def test_random_graphs_vs_oracle(gpu, seed):
 # ---------------------------------------------------------------------------
 # negative cycles (config 5 in miniature and at scale)
 # ---------------------------------------------------------------------------
-def test_negative_cycles_rmat(gpu):
+def test_negative_cycles_rmat(gpu, frontier_mode):
     base, _ = G.johnson_reweight(G.rmat_graph(12, 16), pseed=3)
     dv, _, st = P.govm_sssp(base, 0)
     od, _, o = O.jacobi_sssp(base, 0, "govm", vtype="int32")
@@ -276,6 +284,7 @@ def test_negative_cycle_cap_without_early_exit(gpu):
         _, _, st = P.govm_sssp(g, s)
         _, _, o = O.jacobi_sssp(g, s, "govm", vtype="float64")
         assert st.negative_cycle and o["negative_cycle"] and st.outer_steps == g.n == o["outer_steps"]
+        assert counters(st) == oracle_counters(o)
 
 
 def _ref_like_negative_cycle(seed, n=40):
@@ -283,7 +292,7 @@ def _ref_like_negative_cycle(seed, n=40):
     m = 4 * n
     u, v = rng.integers(0, n, m), rng.integers(0, n, m)
     w = rng.uniform(0, 2, m)
-    cyc = rng.choice(n, size=3, replace=False)
+    cyc = 1 + rng.choice(n - 1, size=3, replace=False)  # avoid the source: the cap path, not the guard
     eu = [cyc[0], cyc[1], cyc[2], 0]
     ev = [cyc[1], cyc[2], cyc[0], cyc[0]]
     ew = [0.5, 0.5, -1.5, 1.0]
@@ -293,7 +302,7 @@ def _ref_like_negative_cycle(seed, n=40):
 # ---------------------------------------------------------------------------
 # larger graphs: exact vs oracle, properties at full scale
 # ---------------------------------------------------------------------------
-def test_rmat16_vs_oracle(gpu):
+def test_rmat16_vs_oracle(gpu, frontier_mode):
     g = G.rmat_graph(16, 16, weights="f32")
     for precision, vt in (("fp32", "float32"), ("fp64", "float64")):
         dv, _, st = P.govm_sssp(g, 0, precision=precision)
@@ -305,7 +314,7 @@ def test_rmat16_vs_oracle(gpu):
     assert same(dv.dist, gd)
 
 
-def test_grid_vs_oracle(gpu):
+def test_grid_vs_oracle(gpu, frontier_mode):
     g = G.grid_graph(128, 128)
     for algo in ("govm", "gsvm"):
         dv, _, st = P.SOLVERS[algo](g, 0)
