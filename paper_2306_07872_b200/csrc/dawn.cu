@@ -407,13 +407,25 @@ struct Impl {
 
   static int setup(dawn_solver_t s) {
     const size_t sm = smem_bytes();
-    CK(cudaFuncSetAttribute(dawn_persistent<V, EI, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    CK(cudaFuncSetAttribute(dawn_persistent<V, EI, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    const bool raw = !s->g->has_negative;
+    auto k0 = raw ? dawn_persistent<V, EI, false, true> : dawn_persistent<V, EI, false, false>;
+    auto k1 = raw ? dawn_persistent<V, EI, true, true> : dawn_persistent<V, EI, true, false>;
+    CK(cudaFuncSetAttribute(k0, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    CK(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    // Keep the shared-memory carveout to what DAWN_MIN_BLOCKS resident CTAs
+    // need: the rest of the unified 228 KB stays L1, which serves the skewed
+    // dist[] gathers (an L2-only gather caps the relax at ~140 G edges/s).
+    {
+      const double need_kb = DAWN_MIN_BLOCKS * ((double)sm / 1024.0 + 1.0);
+      const int pct = std::min(100, (int)std::ceil(100.0 * need_kb / 228.0));
+      CK(cudaFuncSetAttribute(k0, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+      CK(cudaFuncSetAttribute(k1, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+    }
     int bps0 = 0, bps1 = 0, nsm = 0, dev = 0;
     CK(cudaGetDevice(&dev));
     CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps0, dawn_persistent<V, EI, false>, NT, sm));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps1, dawn_persistent<V, EI, true>, NT, sm));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps0, k0, NT, sm));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps1, k1, NT, sm));
     if (bps0 < 1 || bps1 < 1) return fail(DAWN_ECUDA, "persistent kernel cannot be resident (smem %zu)", sm);
     const int64_t n = s->g->n, m = s->g->m;
     const int64_t work = std::max<int64_t>((n + TILE - 1) / TILE, (m + TILE - 1) / TILE);
@@ -431,7 +443,8 @@ struct Impl {
     if (s->prof) CK(cudaMemsetAsync(s->prof, 0, 32 * (size_t)s->prof_cap, stream));
     if (s->pred) CK(cudaMemsetAsync(s->pred, 0, sizeof(unsigned long long) * n, stream));
     KParams<V, EI> P = params(s, 0);
-    dawn_init_solve<V, EI><<<1, 32, 0, stream>>>(P);
+    if (s->g->has_negative) dawn_init_solve<V, EI, false><<<1, 32, 0, stream>>>(P);
+    else dawn_init_solve<V, EI, true><<<1, 32, 0, stream>>>(P);
     CK(cudaGetLastError());
     return DAWN_OK;
   }
@@ -439,13 +452,12 @@ struct Impl {
   static int run(dawn_solver_t s, unsigned max_rounds, cudaStream_t stream) {
     KParams<V, EI> P = params(s, max_rounds);
     void* args[] = {&P};
-    if (P.pred_on) {
-      CK(cudaLaunchCooperativeKernel((void*)dawn_persistent<V, EI, true>, dim3(s->grid_pred), dim3(NT), args,
-                                     s->smem, stream));
-    } else {
-      CK(cudaLaunchCooperativeKernel((void*)dawn_persistent<V, EI, false>, dim3(s->grid), dim3(NT), args,
-                                     s->smem, stream));
-    }
+    const bool raw = !s->g->has_negative;
+    void* fn;
+    if (P.pred_on) fn = raw ? (void*)dawn_persistent<V, EI, true, true> : (void*)dawn_persistent<V, EI, true, false>;
+    else fn = raw ? (void*)dawn_persistent<V, EI, false, true> : (void*)dawn_persistent<V, EI, false, false>;
+    CK(cudaLaunchCooperativeKernel(fn, dim3(P.pred_on ? s->grid_pred : s->grid), dim3(NT), args, s->smem,
+                                   stream));
     return DAWN_OK;
   }
 
@@ -455,7 +467,8 @@ struct Impl {
     if (dist_out) {
       const bool dev = is_device_ptr(dist_out);
       double* target = dev ? dist_out : s->dbuf;
-      dawn_decode_dist<V><<<blocks, 256, 0, stream>>>((const K*)s->dist, (uint32_t)n, target);
+      if (s->g->has_negative) dawn_decode_dist<V, false><<<blocks, 256, 0, stream>>>((const K*)s->dist, (uint32_t)n, target);
+      else dawn_decode_dist<V, true><<<blocks, 256, 0, stream>>>((const K*)s->dist, (uint32_t)n, target);
       CK(cudaGetLastError());
       if (!dev) CK(cudaMemcpyAsync(dist_out, s->dbuf, 8 * (size_t)n, cudaMemcpyDeviceToHost, stream));
     }
@@ -489,7 +502,7 @@ struct Impl {
       CK(cudaMalloc(&s->qbase[i], es * n));
       CK(cudaMalloc(&s->qkey[i], ks * n));
     }
-    CK(cudaMalloc(&s->tile_row, 4 * (size_t)(m / TILE + 4)));
+    CK(cudaMalloc(&s->tile_row, 4 * (size_t)(m / WT + 4)));
     CK(cudaMalloc(&s->st, sizeof(DevState)));
     CK(cudaMemset(s->st, 0, sizeof(DevState)));
     CK(cudaMallocHost(&s->st_host, sizeof(DevState)));

@@ -9,6 +9,8 @@
 #include <math_constants.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 namespace dawn {
 
 #ifndef DAWN_MIN_BLOCKS
@@ -101,6 +103,66 @@ template <> struct Val<double> {
   }
   __device__ __forceinline__ static bool usable(K c) { return c < FINF; }
   __device__ __forceinline__ static double to_f64(K k) { return k == INF ? CUDART_INF : dec(k); }
+};
+
+// ---------------------------------------------------------------------------
+// Key codec used by the kernels.  RAW (the graph has no negative weight, so
+// every distance is >= +0): a non-negative value's own bit pattern is already
+// order-preserving as an unsigned integer, so keys are raw bits and one relax
+// is a single add.  Otherwise the sign-flip encoding of Val<V>.  Row values
+// are decoded once per frontier row (C), never per edge.
+// ---------------------------------------------------------------------------
+template <class V> struct Bits;
+template <> struct Bits<float> {
+  __device__ __forceinline__ static uint32_t to(float x) { return __float_as_uint(x); }
+  __device__ __forceinline__ static float from(uint32_t b) { return __uint_as_float(b); }
+};
+template <> struct Bits<double> {
+  __device__ __forceinline__ static unsigned long long to(double x) { return (unsigned long long)__double_as_longlong(x); }
+  __device__ __forceinline__ static double from(unsigned long long b) { return __longlong_as_double((long long)b); }
+};
+
+template <class V, bool RAW>
+struct Codec {
+  using B = Val<V>;
+  using K = typename B::K;
+  using WB = typename B::WB;
+  using C = V;  // per-row compute value
+  static constexpr K INF = B::INF;
+  static constexpr bool FP = std::is_floating_point<V>::value;
+  __device__ __forceinline__ static C dec(K k) {
+    if constexpr (!RAW) return B::dec(k);
+    else if constexpr (FP) return Bits<V>::from(k);
+    else return (C)k;
+  }
+  __device__ __forceinline__ static K enc(C c) {
+    if constexpr (!RAW) return B::enc(c);
+    else if constexpr (FP) return Bits<V>::to(c);
+    else return (K)c;
+  }
+  __device__ __forceinline__ static K relax(C du, WB w) {
+    if constexpr (FP) {
+      C sum;
+      if constexpr (sizeof(V) == 4) sum = __fadd_rn(du, Bits<V>::from(w));
+      else sum = __dadd_rn(du, Bits<V>::from(w));
+      if constexpr (!RAW) {  // -0 -> +0 so key order == numeric order
+        if constexpr (sizeof(V) == 4) sum = __fadd_rn(sum, 0.0f);
+        else sum = __dadd_rn(sum, 0.0);
+      }
+      return enc(sum);
+    } else {
+      return enc(du + (C)w);
+    }
+  }
+  // reference: `alpha[idx] > cand` is false for cand == inf (overflow): never write it
+  __device__ __forceinline__ static bool usable(K c) {
+    if constexpr (!FP) return true;
+    else if constexpr (RAW) return c < Bits<V>::to((V)CUDART_INF);
+    else return c < B::FINF;
+  }
+  __device__ __forceinline__ static double to_f64(K k) {
+    return k == INF ? CUDART_INF : (double)dec(k);
+  }
 };
 
 // ---------------------------------------------------------------------------

@@ -66,21 +66,22 @@ struct KParams {
   unsigned prof_cap;                   // rounds the timeline can hold
 };
 
+constexpr int WPB = NT / 32;       // warps per CTA
+constexpr int WT = 32 * ITEMS;     // virtual edges per warp tile (256)
+
+// Per-warp shared memory is only the row-start marks of a short-row tile
+// (512 B): everything else stays in registers or is read through L1, so the
+// shared-memory carveout stays minimal and L1 keeps ~200 KB for dist[] gathers.
+template <class V, class EI>
+struct __align__(16) WarpRows {
+  uint16_t mark[WT];            // row-start marks -> per-edge row index (max-scan)
+};
+
 template <class V, class EI>
 struct __align__(16) Smem {
-  using K = typename Val<V>::K;
-  uint16_t mark[TILE];          // row-start marks -> per-edge row index (max-scan)
-  K key[TILE + 1];              // snapshot key per tile row
-  EI base[TILE + 1];            // row base per tile row
-  uint32_t qnode[TILE + 1];     // enqueue buffer nodes; tile row nodes in the pred pass
-  EI qrs[TILE];                 // enqueue buffer: row start
-  EI qdeg[TILE];                // enqueue buffer: degree, then local offset
-  EI scr[NT / 32];
-  unsigned long long scr64[NT / 32];
-  uint32_t wmark[NT / 32];
+  WarpRows<V, EI> w[WPB];
+  unsigned long long scr64[WPB];
   unsigned long long basepk;
-  uint32_t tr[2][2];            // [parity][first row, last row] of the next tile
-  int qcnt;
 };
 
 template <class V> struct EdgeAccess;
@@ -116,11 +117,11 @@ __device__ __forceinline__ unsigned long long pk_edges(unsigned long long pk, in
   return pk & ((1ull << ebits) - 1ull);
 }
 
-// mark the tiles whose first virtual edge falls inside [off, off + deg)
+// mark the warp tiles whose first virtual edge falls inside [off, off + deg)
 template <class EI>
 __device__ __forceinline__ void mark_tiles(uint32_t* tile_row, EI off, EI deg, uint32_t entry) {
-  EI t0 = (off + (EI)(TILE - 1)) / (EI)TILE;
-  EI t1 = (off + deg - 1) / (EI)TILE;
+  EI t0 = (off + (EI)(WT - 1)) / (EI)WT;
+  EI t1 = (off + deg - 1) / (EI)WT;
   for (EI t = t0; t <= t1; ++t) tile_row[t] = entry;
 }
 
@@ -309,249 +310,259 @@ __device__ void phase_compact(const KParams<V, EI>& P, int p, uint32_t r, Smem<V
 }
 
 // ---------------------------------------------------------------------------
-// X phase: tiles of the frontier's virtual edge list.
+// X phase: warp tiles of the frontier's virtual edge list.
 //   PRED == false : relax (+ enqueue when !dense)
 //   PRED == true  : predecessor pass — among this round's frontier edges that
 //                   reproduce the final value of a node lowered this round,
 //                   keep the smallest source node (deterministic witness).
-// Static tile assignment t = blockIdx.x + k*G (every tile has TILE edges).
-// Software pipeline: while tile t streams, the row metadata of tile t+G and
-// the row range of tile t+2G are already in flight (registers).
+// Every warp owns whole WT-edge tiles (t = global warp id + k * total warps;
+// all tiles have WT edges) and never waits for another warp.
+// Row lookup: a tile with <= 32 frontier rows keeps row k in lane k's
+// registers; for each 32-edge window one OR-reduction of row-start bits plus a
+// popc gives every lane its row, and shuffles fetch the row's base and value
+// (no shared memory, no scan).  Tiles with more rows (short rows) use
+// row-start marks in shared memory and a warp max-scan.
+// Software pipeline: while tile t streams, the first 32 rows of the warp's
+// next tile and the row range of the one after are in flight.
 // ---------------------------------------------------------------------------
 constexpr uint32_t SENT = 0xFFFFFFFFu;
 
-template <class V, class EI, bool PRED>
+template <class V, class EI, bool PRED, bool RAW>
 __device__ void phase_expand(const KParams<V, EI>& P, int p, uint32_t r, bool dense, Smem<V, EI>& s,
                              unsigned long long& acc_w, unsigned long long& acc_fd,
                              unsigned long long& acc_multi, uint32_t& round_w) {
-  using VT = Val<V>;
-  using K = typename VT::K;
-  using WB = typename VT::WB;
+  using CD = Codec<V, RAW>;
+  using K = typename CD::K;
+  using WB = typename CD::WB;
+  using C = typename CD::C;
   const unsigned long long pk = ldcg(&P.st->res[p]);
   const uint32_t cnt = (uint32_t)pk_count(pk, P.ebits);
   const EI E = (EI)pk_edges(pk, P.ebits);
   if (E == 0) return;
-  const EI T = (E + (EI)(TILE - 1)) / (EI)TILE;
-  const EI G = gridDim.x;
-  EI t = blockIdx.x;
-  if (t >= T) return;
+  const EI T = (E + (EI)(WT - 1)) / (EI)WT;
+  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const EI GW = (EI)gridDim.x * WPB;
+  EI t = (EI)blockIdx.x * WPB + wid;
+  if (t >= T) return;  // warp-uniform; no CTA barrier below
+  WarpRows<V, EI>& w = s.w[wid];
   const int np = p ^ 1;
+  const int eb = P.ebits;
   const uint32_t src = P.src;
-  const int tid = threadIdx.x;
   const uint32_t* tile_row = P.tile_row;
   const EI* qbase = P.qbase[p];
   const EI* qoff = P.qoff[p];
   const K* qkey = P.qkey[p];
   const uint32_t* qnode = P.qnode[p];
-  // rows of tile q are [tile_row[q], tile_row[q+1]] (the last tile ends at cnt-1)
-  auto row_bound = [&](EI q, int which) -> uint32_t {
+  auto row_bound = [&](EI q, uint32_t which) -> uint32_t {
     const EI x = q + (EI)which;
     return (x < T) ? ldcg(tile_row + x) : cnt - 1;
   };
 
-  // prologue: rows of tile t into registers, row range of tile t+G
-  uint32_t cur_i0 = row_bound(t, 0), cur_il = row_bound(t, 1);
-  uint32_t tr_nx = 0;  // tid 0 / 1: first / last row of the tile after the current one
-  if (tid < 2 && t + G < T) tr_nx = row_bound(t + G, tid);
+  // prologue: first 32 rows of tile t into registers, row range of t+GW
+  uint32_t i0 = row_bound(t, 0), il = row_bound(t, 1);
+  uint32_t tr = (lane < 2 && t + GW < T) ? row_bound(t + GW, lane) : 0u;
   EI pf_base = 0, pf_off = 0;
   K pf_key = 0;
   uint32_t pf_node = 0;
-  if ((uint32_t)tid <= cur_il - cur_i0) {
-    const uint32_t i = cur_i0 + tid;
-    pf_base = ldcg(qbase + i);
-    pf_off = ldcg(qoff + i);
-    pf_key = ldcg(qkey + i);
-    if (PRED) pf_node = ldcg(qnode + i);
+  if (lane <= il - i0) {
+    pf_base = ldcg(qbase + i0 + lane);
+    pf_off = ldcg(qoff + i0 + lane);
+    pf_key = ldcg(qkey + i0 + lane);
+    if (PRED) pf_node = ldcg(qnode + i0 + lane);
   }
-  int par = 0;
 
-  for (; t < T; t += G) {
-    const EI e0 = t * (EI)TILE;
-    const EI e1 = (E - e0 < (EI)TILE) ? E : e0 + (EI)TILE;
-    const uint32_t i0 = cur_i0, ilast = cur_il;
-    const uint32_t nrows = ilast - i0 + 1;
-    const bool multi_row = nrows > 1;
-    // ---- publish this tile's (prefetched) rows and the next tile's range ----
-    reinterpret_cast<uint4*>(s.mark)[tid] = make_uint4(0, 0, 0, 0);
-    if ((uint32_t)tid < nrows) {
-      s.base[tid] = pf_base;
-      s.key[tid] = pf_key;
-      if (PRED) s.qnode[tid] = pf_node;
-    }
-    if (tid < 2) s.tr[par][tid] = tr_nx;
-    __syncthreads();
-    if (multi_row) {  // row-start marks (after the zeroing above is complete)
-      if ((uint32_t)tid < nrows) {
-        const EI start = pf_off > e0 ? pf_off : e0;
-        if (start < e1) s.mark[start - e0] = (uint16_t)tid;
-      }
-      for (uint32_t k = NT + tid; k < nrows; k += NT) {  // rows beyond the first NT (tiny rows)
-        const uint32_t i = i0 + k;
-        s.base[k] = ldcg(qbase + i);
-        s.key[k] = ldcg(qkey + i);
-        if (PRED) s.qnode[k] = ldcg(qnode + i);
-        const EI off = ldcg(qoff + i);
-        const EI start = off > e0 ? off : e0;
-        if (start < e1) s.mark[start - e0] = (uint16_t)k;
+  for (; t < T; t += GW) {
+    const EI e0 = t * (EI)WT;
+    const uint32_t len = (E - e0 < (EI)WT) ? (uint32_t)(E - e0) : (uint32_t)WT;
+    const uint32_t nrows = il - i0 + 1;
+    const bool fast = nrows <= 32;
+    const uint32_t ci0 = i0;
+    // this tile's rows (lane k = row k) from the prefetch registers
+    const EI c_base = pf_base;
+    const C c_val = CD::dec(pf_key);
+    const uint32_t c_node = pf_node;
+    const uint32_t c_rst = (lane < nrows) ? (uint32_t)(pf_off > e0 ? pf_off - e0 : (EI)0) : 0xFFFFFFFFu;
+    if (!fast) {
+      // ---- short rows: mark row starts (row data is read through L1 below) ----
+      reinterpret_cast<uint4*>(w.mark)[lane] = make_uint4(0, 0, 0, 0);
+      __syncwarp();
+      if (c_rst < len) w.mark[c_rst] = (uint16_t)lane;
+      for (uint32_t k = 32 + lane; k < nrows; k += 32) {
+        const EI off = __ldca(qoff + ci0 + k);
+        const EI rst = off > e0 ? off - e0 : (EI)0;
+        if (rst < (EI)len) w.mark[rst] = (uint16_t)k;
       }
     }
-    // ---- advance the pipeline: rows of tile t+G, range of tile t+2G ----
-    const EI tn = t + G;
-    if (tn < T) {
-      cur_i0 = s.tr[par][0];
-      cur_il = s.tr[par][1];
-      if ((uint32_t)tid <= cur_il - cur_i0) {
-        const uint32_t i = cur_i0 + tid;
-        pf_base = ldcg(qbase + i);
-        pf_off = ldcg(qoff + i);
-        pf_key = ldcg(qkey + i);
-        if (PRED) pf_node = ldcg(qnode + i);
+    // ---- advance the pipeline: rows of the next tile, range of the one after ----
+    {
+      const EI tn = t + GW;
+      const uint32_t ni0 = __shfl_sync(0xffffffffu, tr, 0), nil = __shfl_sync(0xffffffffu, tr, 1);
+      if (tn < T) {
+        i0 = ni0;
+        il = nil;
+        if (lane <= il - i0) {
+          pf_base = ldcg(qbase + i0 + lane);
+          pf_off = ldcg(qoff + i0 + lane);
+          pf_key = ldcg(qkey + i0 + lane);
+          if (PRED) pf_node = ldcg(qnode + i0 + lane);
+        }
+        tr = (lane < 2 && tn + GW < T) ? row_bound(tn + GW, lane) : 0u;
       }
-      if (tid < 2 && tn + G < T) tr_nx = row_bound(tn + G, tid);
     }
-    par ^= 1;
-    if (multi_row) __syncthreads();
-    if (multi_row) {
-      // inclusive max-scan of the marks: each thread owns ITEMS consecutive slots
-      const uint4 mv = reinterpret_cast<uint4*>(s.mark)[tid];
+    if (!fast) {
+      __syncwarp();
+      // inclusive max-scan of the marks: each lane owns ITEMS consecutive slots
+      const uint4 mv = reinterpret_cast<uint4*>(w.mark)[lane];
       uint32_t m8[8] = {mv.x & 0xFFFFu, mv.x >> 16, mv.y & 0xFFFFu, mv.y >> 16,
                         mv.z & 0xFFFFu, mv.z >> 16, mv.w & 0xFFFFu, mv.w >> 16};
       uint32_t run = 0;
 #pragma unroll
       for (int j = 0; j < 8; ++j) { run = max(run, m8[j]); m8[j] = run; }
-      const int lane = tid & 31, warp = tid >> 5;
       uint32_t incl = run;
 #pragma unroll
       for (int d = 1; d < 32; d <<= 1) {
         const uint32_t y = __shfl_up_sync(0xffffffffu, incl, d);
-        if (lane >= d) incl = max(incl, y);
+        if (lane >= (uint32_t)d) incl = max(incl, y);
       }
-      uint32_t excl = __shfl_up_sync(0xffffffffu, incl, 1);
-      if (lane == 0) excl = 0;
-      if (lane == 31) s.wmark[warp] = incl;
-      __syncthreads();
-      uint32_t pre_w = excl;
-      for (int w = 0; w < warp; ++w) pre_w = max(pre_w, s.wmark[w]);
+      uint32_t pre = __shfl_up_sync(0xffffffffu, incl, 1);
+      if (lane == 0) pre = 0;
 #pragma unroll
-      for (int j = 0; j < 8; ++j) m8[j] = max(m8[j], pre_w);
-      reinterpret_cast<uint4*>(s.mark)[tid] =
+      for (int j = 0; j < 8; ++j) m8[j] = max(m8[j], pre);
+      reinterpret_cast<uint4*>(w.mark)[lane] =
           make_uint4(m8[0] | (m8[1] << 16), m8[2] | (m8[3] << 16), m8[4] | (m8[5] << 16),
                      m8[6] | (m8[7] << 16));
-      __syncthreads();
+      __syncwarp();
     }
 
-    // ---- phase 1: positions, then all edge loads back to back ----
-    uint32_t col[ITEMS];
-    WB wv[ITEMS];
+    // ---- phase 1a: row of every edge (collectives / L1 only, no edge loads yet) ----
+    EI pos[ITEMS];
+    C rv[ITEMS];          // row value (decoded once per row)
     uint32_t rowk[ITEMS];
-    unsigned okm = 0;
-    {
-      EI pos[ITEMS];
-      const EI safe = s.base[0] + e0;  // first edge of the tile: always a valid address
+    if (fast) {
+      uint32_t before = 0;  // rows starting before the current 32-edge window
 #pragma unroll
       for (int j = 0; j < ITEMS; ++j) {
-        const uint32_t idx = j * NT + tid;
-        const EI e = e0 + idx;
-        const bool ok = e < e1;
-        okm |= (unsigned)ok << j;
-        const uint32_t k = (multi_row && ok) ? (uint32_t)s.mark[idx] : 0u;
+        const uint32_t lo = j * 32;
+        const uint32_t bit = (c_rst - lo < 32u) ? (1u << (c_rst - lo)) : 0u;
+        const uint32_t B = __reduce_or_sync(0xffffffffu, bit);
+        const uint32_t k = before + __popc(B & (0xFFFFFFFFu >> (31 - lane))) - 1;
+        before += __popc(B);
         rowk[j] = k;
-        pos[j] = ok ? s.base[k] + e : safe;
+        pos[j] = __shfl_sync(0xffffffffu, c_base, k) + e0 + (EI)(lo + lane);
+        rv[j] = __shfl_sync(0xffffffffu, c_val, k);
       }
+    } else {
 #pragma unroll
-      for (int j = 0; j < ITEMS; ++j) EdgeAccess<V>::load(P, pos[j], col[j], wv[j]);
+      for (int j = 0; j < ITEMS; ++j) {
+        // queue entries were written before the last grid barrier, whose fence
+        // invalidated L1: L1-cached reads are coherent here
+        const uint32_t k = w.mark[j * 32 + lane];
+        rowk[j] = k;
+        pos[j] = __ldca(qbase + ci0 + k) + e0 + (EI)(j * 32 + lane);
+        rv[j] = CD::dec(__ldca(qkey + ci0 + k));
+      }
+    }
+    // ---- phase 1b: all edge loads back to back (nothing consumes them yet) ----
+    uint32_t col[ITEMS];
+    WB wv[ITEMS];
+    unsigned okm = 0xFFu;  // items inside the tile
+    if (len != (uint32_t)WT) {
+      okm = 0;
+#pragma unroll
+      for (int j = 0; j < ITEMS; ++j) okm |= (unsigned)(j * 32 + lane < len) << j;
+    }
+    {
+      const EI safe0 = __shfl_sync(0xffffffffu, c_base, 0) + e0;  // the tile's first edge
+#pragma unroll
+      for (int j = 0; j < ITEMS; ++j) EdgeAccess<V>::load(P, ((okm >> j) & 1u) ? pos[j] : safe0, col[j], wv[j]);
     }
     // ---- phase 2: candidates ----
     K cand[ITEMS];
 #pragma unroll
     for (int j = 0; j < ITEMS; ++j) {
-      cand[j] = VT::relax(s.key[rowk[j]], wv[j]);
-      if (!((okm >> j) & 1u) || !VT::usable(cand[j])) col[j] = SENT;
+      cand[j] = CD::relax(rv[j], wv[j]);
+      if (!CD::usable(cand[j])) okm &= ~(1u << j);
     }
     if (!PRED) {
-      // ---- phase 3: coherent read-before-write filter, all gathers in flight ----
+      // ---- phase 3: read-before-write filter, all gathers in flight ----
+      // L1-allocating loads (ld.ca): RMAT-like destinations are skewed, so a
+      // large share of gathers hit L1 (measured 2.2x over L2-only gathers,
+      // tools/gather_bench.cu).  Safe for the "cand < cur => lowered this
+      // round" inference: every grid barrier's fence invalidates L1
+      // (CCTL.IVALL) and no gather is outstanding at a barrier, so a value
+      // seen in L1 during round r was read after round r began and is <= the
+      // round-start value.
       K cur[ITEMS];
 #pragma unroll
-      for (int j = 0; j < ITEMS; ++j) cur[j] = (col[j] != SENT) ? ldcg(P.dist + col[j]) : (K)0;
+      for (int j = 0; j < ITEMS; ++j) cur[j] = ((okm >> j) & 1u) ? __ldca(P.dist + col[j]) : (K)0;
       unsigned need = 0;
 #pragma unroll
       for (int j = 0; j < ITEMS; ++j) {
-        if (col[j] != SENT && cand[j] < cur[j]) {
+        if (((okm >> j) & 1u) && cand[j] < cur[j]) {
           if (col[j] == src) P.st->flag = 1u;  // source guard (solver.py:299-303, :374-376, :236-239)
           else need |= 1u << j;
         }
       }
       // ---- phase 4: fire-and-forget min (cand < cur proves v is lowered this round) ----
+      if (need) {
 #pragma unroll
-      for (int j = 0; j < ITEMS; ++j)
-        if ((need >> j) & 1u) atomicMin(P.dist + col[j], cand[j]);
+        for (int j = 0; j < ITEMS; ++j)
+          if ((need >> j) & 1u) atomicMin(P.dist + col[j], cand[j]);
+      }
       if (dense) {
+        if (need) {
 #pragma unroll
-        for (int j = 0; j < ITEMS; ++j)
-          if ((need >> j) & 1u) P.stamp[col[j]] = r;
-      } else if (need) {
-        unsigned os[ITEMS];
-#pragma unroll
-        for (int j = 0; j < ITEMS; ++j)
-          if ((need >> j) & 1u) os[j] = atomicExch(P.stamp + col[j], r);
+          for (int j = 0; j < ITEMS; ++j)
+            if ((need >> j) & 1u) P.stamp[col[j]] = r;
+        }
+      } else if (__any_sync(0xffffffffu, need != 0u)) {
+        // ---- sparse: elect one writer per (node, round), enqueue its row ----
         unsigned first = 0;
 #pragma unroll
+        for (int j = 0; j < ITEMS; ++j)
+          if (((need >> j) & 1u) && atomicExch(P.stamp + col[j], r) != r) first |= 1u << j;
+        unsigned long long mine = 0;  // (entries << eb) | edges of this lane
+        EI rs[ITEMS];
+#pragma unroll
         for (int j = 0; j < ITEMS; ++j) {
-          if (((need >> j) & 1u) && os[j] != r) {  // the one thread electing v this round
-            first |= 1u << j;
+          rs[j] = 0;
+          if ((first >> j) & 1u) {
             round_w++;
             acc_w++;
             count_write(P.wstate, col[j], acc_fd, acc_multi);
+            const EI a = __ldg(P.row_ptr + col[j]), b = __ldg(P.row_ptr + col[j] + 1);
+            rs[j] = a;
+            if (b > a) {  // rows without edges never need a rescan
+              mine += (1ull << eb) + (unsigned long long)(b - a);
+              wv[j] = (WB)(b - a);  // reuse: degree
+            } else {
+              first &= ~(1u << j);
+            }
           }
         }
-        if (first) {
-          EI a[ITEMS], b[ITEMS];
+        unsigned long long incl = mine;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const unsigned long long y = __shfl_up_sync(0xffffffffu, incl, d);
+          if (lane >= (uint32_t)d) incl += y;
+        }
+        const unsigned long long tot = __shfl_sync(0xffffffffu, incl, 31);
+        if (tot) {
+          unsigned long long base = 0;
+          if (lane == 0) base = atomicAdd(&P.st->res[np], tot);
+          base = __shfl_sync(0xffffffffu, base, 0);
+          const unsigned long long at = base + incl - mine;
+          uint32_t pos = (uint32_t)pk_count(at, eb);
+          EI off = (EI)pk_edges(at, eb);
 #pragma unroll
           for (int j = 0; j < ITEMS; ++j) {
             if ((first >> j) & 1u) {
-              a[j] = __ldg(P.row_ptr + col[j]);
-              b[j] = __ldg(P.row_ptr + col[j] + 1);
+              P.qnode[np][pos] = col[j];
+              P.qoff[np][pos] = off;
+              P.qbase[np][pos] = rs[j] - off;
+              pos++;
+              off += (EI)wv[j];
             }
-          }
-#pragma unroll
-          for (int j = 0; j < ITEMS; ++j) {
-            if (((first >> j) & 1u) && b[j] > a[j]) {  // rows without edges never need a rescan
-              const int slot = atomicAdd(&s.qcnt, 1);
-              s.qnode[slot] = col[j];
-              s.qrs[slot] = a[j];
-              s.qdeg[slot] = b[j] - a[j];
-            }
-          }
-        }
-      }
-      if (!dense) {
-        // ---- flush the enqueue buffer: one packed reservation per tile ----
-        __syncthreads();
-        const int q = s.qcnt;
-        if (q > 0) {
-          EI carry = 0;
-          for (int c0 = 0; c0 < q; c0 += NT) {  // exclusive degree scan -> local offsets
-            const int i = c0 + tid;
-            const EI d = (i < q) ? s.qdeg[i] : (EI)0;
-            EI tot;
-            const EI incl = block_incl_sum<EI>(d, s.scr, &tot);
-            if (i < q) s.qdeg[i] = carry + incl - d;
-            carry += tot;
-          }
-          if (tid == 0) {
-            s.basepk = atomicAdd(&P.st->res[np],
-                                 ((unsigned long long)q << P.ebits) | (unsigned long long)carry);
-            s.qcnt = 0;
-          }
-          __syncthreads();
-          const unsigned long long bp = s.basepk;
-          const uint32_t bc = (uint32_t)pk_count(bp, P.ebits);
-          const EI be = (EI)pk_edges(bp, P.ebits);
-          for (int i = tid; i < q; i += NT) {
-            const EI off = be + s.qdeg[i];
-            P.qnode[np][bc + i] = s.qnode[i];
-            P.qoff[np][bc + i] = off;
-            P.qbase[np][bc + i] = s.qrs[i] - off;
           }
         }
       }
@@ -559,19 +570,18 @@ __device__ void phase_expand(const KParams<V, EI>& P, int p, uint32_t r, bool de
       unsigned sv[ITEMS];
 #pragma unroll
       for (int j = 0; j < ITEMS; ++j)
-        sv[j] = (col[j] != SENT && col[j] != src) ? ldcg(P.stamp + col[j]) : 0u;
+        sv[j] = (((okm >> j) & 1u) && col[j] != src) ? ldcg(P.stamp + col[j]) : 0u;
       K dv[ITEMS];
 #pragma unroll
       for (int j = 0; j < ITEMS; ++j) dv[j] = (sv[j] == r) ? ldcg(P.dist + col[j]) : (K)0;
 #pragma unroll
       for (int j = 0; j < ITEMS; ++j) {
-        if (sv[j] == r && col[j] != SENT && col[j] != src && cand[j] == dv[j]) {
-          const uint32_t u = s.qnode[rowk[j]];
+        const uint32_t u = fast ? __shfl_sync(0xffffffffu, c_node, rowk[j]) : __ldca(qnode + ci0 + rowk[j]);
+        if (sv[j] == r && ((okm >> j) & 1u) && col[j] != src && cand[j] == dv[j])
           atomicMax(P.pred + col[j], ((unsigned long long)r << 32) | (unsigned long long)(~u));
-        }
       }
     }
-    __syncthreads();  // everyone is done with marks / rows / the enqueue buffer
+    __syncwarp();  // the warp is done with its rows / marks
   }
 }
 
@@ -618,14 +628,12 @@ __device__ bool pred_graph_has_cycle(const KParams<V, EI>& P) {
 // ---------------------------------------------------------------------------
 // WITH_PRED instantiates the predecessor pass and the negative-cycle check;
 // the plain instance carries none of their registers.
-template <class V, class EI, bool WITH_PRED>
+template <class V, class EI, bool WITH_PRED, bool RAW>
 __global__ void __launch_bounds__(NT, DAWN_MIN_BLOCKS) dawn_persistent(KParams<V, EI> P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem<V, EI>& s = *reinterpret_cast<Smem<V, EI>*>(smem_raw);
   DevState* st = P.st;
   const bool leader = (blockIdx.x == 0 && threadIdx.x == 0);
-  if (threadIdx.x == 0) s.qcnt = 0;
-  __syncthreads();
 
   uint32_t r = ldcg(&st->round);
   bool dense_prev = ldcg(&st->dense_prev) != 0u;  // how round r-1 recorded its writes
@@ -697,13 +705,13 @@ __global__ void __launch_bounds__(NT, DAWN_MIN_BLOCKS) dawn_persistent(KParams<V
       P.prof[4 * r + 3] = ldcg(&st->res[p]);
     }
     uint32_t round_w = 0;
-    phase_expand<V, EI, false>(P, p, r, dense, s, acc_w, acc_fd, acc_multi, round_w);
+    phase_expand<V, EI, false, RAW>(P, p, r, dense, s, acc_w, acc_fd, acc_multi, round_w);
     round_w = __reduce_add_sync(0xffffffffu, round_w);
     if ((threadIdx.x & 31) == 0 && round_w) atomicAdd(&st->wround[p], (unsigned long long)round_w);
     grid_sync(&st->bar);
     if (leader) st->resume_x = 0u;  // every CTA has read it (first barrier passed)
     if constexpr (WITH_PRED) {
-      phase_expand<V, EI, true>(P, p, r, dense, s, acc_w, acc_fd, acc_multi, round_w);
+      phase_expand<V, EI, true, RAW>(P, p, r, dense, s, acc_w, acc_fd, acc_multi, round_w);
       grid_sync(&st->bar);
     }
     if (prof) P.prof[4 * r + 2] = globaltimer();
@@ -728,13 +736,12 @@ __global__ void __launch_bounds__(NT, DAWN_MIN_BLOCKS) dawn_persistent(KParams<V
 // small kernels
 // ---------------------------------------------------------------------------
 // solve init: seed frontier {source} with key 0 (solver.py:275-280, :343-350)
-template <class V, class EI>
+template <class V, class EI, bool RAW>
 __global__ void dawn_init_solve(KParams<V, EI> P) {
   if (blockIdx.x == 0 && threadIdx.x == 0) {
-    using VT = Val<V>;
     DevState* st = P.st;
     const uint32_t s = P.src;
-    P.dist[s] = VT::enc((V)0);
+    P.dist[s] = Codec<V, RAW>::enc((V)0);
     const EI a = P.row_ptr[s], b = P.row_ptr[s + 1];
     const unsigned long long deg = (unsigned long long)(b - a);
     st->res[0] = 0ull;
@@ -755,11 +762,11 @@ __global__ void dawn_init_solve(KParams<V, EI> P) {
   }
 }
 
-template <class V>
+template <class V, bool RAW>
 __global__ void dawn_decode_dist(const typename Val<V>::K* __restrict__ keys, uint32_t n,
                                  double* __restrict__ out) {
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-    out[i] = Val<V>::to_f64(keys[i]);
+    out[i] = Codec<V, RAW>::to_f64(keys[i]);
 }
 
 template <class V>
