@@ -110,7 +110,8 @@ int dawn_solver_destroy(dawn_solver_t s);
 /* Tuning knobs (results never depend on them):
  *   "dense_edges_per_node" (default 0.5): a round that relaxes at least
  *   value*n edges records its writes as plain stamps and the next frontier is
- *   rebuilt by a coalesced sweep; lighter rounds enqueue written nodes. */
+ *   rebuilt by a coalesced sweep; lighter rounds enqueue written nodes.
+ *   "batch_min_sources" (default 4): dawn_mssp batches k >= value sources. */
 int dawn_solver_tune(dawn_solver_t s, const char* key, double value);
 
 /* One single-source solve: govm_sssp / gsvm_sssp (solver.py:265-399),
@@ -154,12 +155,32 @@ int dawn_solver_round_profile(dawn_solver_t s, uint64_t* out, int64_t cap_rounds
                               void* stream);
 
 /* Multi-source: independent solves from sources[0..k) (host int64 array) in
- * the given order — mssp (solver.py:426-457).  dist_out is a row-major
+ * the given order — mssp (solver.py:426-457).  Uses the batched kernel
+ * (dawn_mssp_batch) when eligible and k >= the "batch_min_sources" tuning
+ * value (default 4), else one persistent solve per source.  dist_out is a row-major
  * float64 [k][n] tile (host or device) or NULL; stats_out a host array of k
  * entries or NULL.  All sources are validated before any work
  * (solver.py:441-443).  One synchronisation at the end. */
 int dawn_mssp(dawn_solver_t s, const int64_t* sources, int64_t k, int algo, unsigned flags,
               double* dist_out, dawn_stats_t* stats_out, void* stream);
+
+/* Batched multi-source solves: up to 32 sources advance
+ * together, one per warp lane, over a node-major [n][32] distance layout, so
+ * each edge is read once per batch and its 32 distance updates are one
+ * coalesced line.  Every per-source distance and counter equals the
+ * single-source dawn_sssp result (same snapshot-Jacobi rounds per lane).
+ * Replaces the per-source loop of mssp / apsp (solver.py:426-457, :460-495).
+ * Eligible when the graph has no negative weight, n >= 2 and DAWN_F_PRED is
+ * not requested (dawn_batch_supported); otherwise DAWN_EUNSUPPORTED.
+ *   dist_out : row-major [k][ld] tile, host or device, or NULL.  out_vtype
+ *              DAWN_F64 (float64 rows, +inf = unreachable, the reference's
+ *              DistanceVector) or DAWN_F32 for a float32 graph (device-
+ *              resident result tiles at half the bytes).
+ *   stats_out: k entries or NULL.  With a device dist_out and NULL stats the
+ *              call is fully asynchronous on `stream`. */
+int dawn_batch_supported(dawn_solver_t s, int algo, unsigned flags, int* out);
+int dawn_mssp_batch(dawn_solver_t s, const int64_t* sources, int64_t k, int algo, unsigned flags,
+                    void* dist_out, int out_vtype, int64_t ld, dawn_stats_t* stats_out, void* stream);
 
 /* Synthetic generators on the device (SURVEY §8(f) row F1 inputs).  They
  * write an edge list (u, v, w) of m edges, deterministic in `seed` through a

@@ -54,6 +54,8 @@ EXPORTS = (
     "dawn_solver_result",
     "dawn_solver_round_profile",
     "dawn_mssp",
+    "dawn_batch_supported",
+    "dawn_mssp_batch",
     "dawn_gen_rmat",
 )
 
@@ -98,6 +100,9 @@ def _declare(L: ctypes.CDLL) -> None:
         "dawn_solver_result": (c_int, [c_void_p, c_void_p, c_void_p, POINTER(Stats), c_void_p]),
         "dawn_solver_round_profile": (c_int, [c_void_p, c_void_p, c_int64, P64, c_void_p]),
         "dawn_mssp": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_uint, c_void_p, c_void_p, c_void_p]),
+        "dawn_batch_supported": (c_int, [c_void_p, c_int, c_uint, POINTER(c_int)]),
+        "dawn_mssp_batch": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_uint, c_void_p, c_int, c_int64,
+                                    c_void_p, c_void_p]),
         "dawn_gen_rmat": (c_int, [c_int, c_int, c_int64, c_double, c_double, c_double, c_uint64, c_int,
                                   c_int64, c_int64, c_uint64, c_void_p, c_void_p, c_void_p, c_void_p]),
     }

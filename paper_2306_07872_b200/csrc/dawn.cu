@@ -21,7 +21,7 @@
 #include <string>
 
 #include "../../include/dawn.h"
-#include "dawn_kernels.cuh"
+#include "dawn_batch.cuh"
 
 using namespace dawn;
 
@@ -94,9 +94,27 @@ struct dawn_solver_s {
   int grid = 1;       // co-resident CTAs of the plain persistent kernel
   int grid_pred = 1;  // ... of the predecessor-tracking instance
   size_t smem = 0;
-  double dense_edges_per_node = 0.5;  // tunable: dense frontier build after rounds relaxing >= this * n edges
+  double dense_edges_per_node = 0.5;
+  double batch_min_sources = 4;       // tunable: dawn_mssp batches when k >= this  // tunable: dense frontier build after rounds relaxing >= this * n edges
   int ebits = 32;
   int logn = 0;
+  // batched multi-source workspace (allocated on first use, kept)
+  bool batch_ready = false;
+  bool last_batch = false;       // the last solve on this solver was a batch (round profile source)
+  void* bd = nullptr;            // K[n][32]
+  uint32_t* bmask[4] = {nullptr, nullptr, nullptr, nullptr};  // nmask, w1, w2, smask
+  uint32_t* bqnode = nullptr;
+  uint32_t* bqmask = nullptr;
+  void* bqoff = nullptr;
+  void* bqbase = nullptr;
+  void* bqkey = nullptr;         // K[n][32]
+  uint32_t* btile = nullptr;
+  BState* bst = nullptr;
+  BState* bst_host = nullptr;    // pinned, one per batch in flight
+  int64_t bst_host_cap = 0;
+  void* bout = nullptr;          // double[32][n] staging for host outputs
+  int bgrid = 1;
+  size_t bsmem = 0;
   // current solve
   int64_t source = -1;
   int algo = 0;
@@ -484,6 +502,115 @@ struct Impl {
     return DAWN_OK;
   }
 
+
+  // ---------------- batched multi-source (dawn_batch.cuh) ----------------
+  static int batch_alloc(dawn_solver_t s) {
+    if (s->batch_ready) return DAWN_OK;
+    const int64_t n = s->g->n, m = s->g->m;
+    const size_t ks = sizeof(K), es = sizeof(EI);
+    CK(cudaMalloc(&s->bd, ks * BL * (size_t)n));
+    for (int i = 0; i < 4; ++i) CK(cudaMalloc(&s->bmask[i], 4 * (size_t)n));
+    CK(cudaMalloc(&s->bqnode, 4 * (size_t)n));
+    CK(cudaMalloc(&s->bqmask, 4 * (size_t)n));
+    CK(cudaMalloc(&s->bqoff, es * (size_t)n));
+    CK(cudaMalloc(&s->bqbase, es * (size_t)n));
+    CK(cudaMalloc(&s->bqkey, ks * BL * (size_t)n));
+    CK(cudaMalloc(&s->btile, 4 * (size_t)(m / BWT + 4)));
+    CK(cudaMalloc(&s->bst, sizeof(BState)));
+    CK(cudaMemset(s->bst, 0, sizeof(BState)));
+    CK(cudaMemset(s->bmask[0], 0, 4 * (size_t)n));
+    auto k = dawn_batch_persistent<V, EI>;
+    const size_t sm = sizeof(BSmem<V, EI>);
+    CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    {
+      const double need_kb = DAWN_MIN_BLOCKS * ((double)(sm + 8 * 1024) / 1024.0 + 1.0);
+      const int pct = std::min(100, (int)std::ceil(100.0 * need_kb / 228.0));
+      CK(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+    }
+    int bps = 0, nsm = 0, dev = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k, NT, sm));
+    if (bps < 1) return fail(DAWN_ECUDA, "batched kernel cannot be resident");
+    const int64_t work = std::max<int64_t>((n + TILE - 1) / TILE, (m + BWT * WPB - 1) / (BWT * WPB));
+    s->bgrid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)bps * nsm, work));
+    s->bsmem = sm;
+    s->batch_ready = true;
+    return DAWN_OK;
+  }
+
+  static BParams<V, EI> bparams(dawn_solver_t s, const int64_t* src, int nl, int algo) {
+    dawn_graph_t g = s->g;
+    BParams<V, EI> P;
+    P.n = (uint32_t)g->n;
+    P.nlanes = (uint32_t)nl;
+    P.row_ptr = (const EI*)g->row_ptr;
+    P.e2 = g->e2;
+    P.ecol = g->ecol;
+    P.ew = g->ew;
+    P.bd = (K*)s->bd;
+    P.nmask = s->bmask[0];
+    P.w1 = s->bmask[1];
+    P.w2 = s->bmask[2];
+    P.smask = s->bmask[3];
+    P.qnode = s->bqnode;
+    P.qmask = s->bqmask;
+    P.qoff = (EI*)s->bqoff;
+    P.qbase = (EI*)s->bqbase;
+    P.qkey = (K*)s->bqkey;
+    P.tile_row = s->btile;
+    P.st = s->bst;
+    for (int l = 0; l < BL; ++l) P.src[l] = l < nl ? (uint32_t)src[l] : 0xFFFFFFFFu;
+    P.ebits = s->ebits;
+    P.algo = algo;
+    P.prof = s->prof;
+    P.prof_cap = s->prof_cap;
+    return P;
+  }
+
+  // one batch of nl <= 32 sources; nmask is all-zero on entry and on exit
+  static int batch_run(dawn_solver_t s, const int64_t* src, int nl, int algo, cudaStream_t stream) {
+    TRY(batch_alloc(s));
+    const int64_t n = s->g->n;
+    CK(cudaMemsetAsync(s->bd, 0xFF, sizeof(K) * BL * (size_t)n, stream));
+    CK(cudaMemsetAsync(s->bmask[1], 0, 4 * (size_t)n, stream));
+    CK(cudaMemsetAsync(s->bmask[2], 0, 4 * (size_t)n, stream));
+    CK(cudaMemsetAsync(s->bmask[3], 0, 4 * (size_t)n, stream));
+    if (s->prof) CK(cudaMemsetAsync(s->prof, 0, 32 * (size_t)s->prof_cap, stream));
+    BParams<V, EI> P = bparams(s, src, nl, algo);
+    dawn_batch_init<V, EI><<<1, 32, 0, stream>>>(P);
+    CK(cudaGetLastError());
+    void* args[] = {&P};
+    CK(cudaLaunchCooperativeKernel((void*)dawn_batch_persistent<V, EI>, dim3(s->bgrid), dim3(NT), args, s->bsmem,
+                                   stream));
+    return DAWN_OK;
+  }
+
+  // decode the batch into rows [nl][ld] of double (out_vt F64) or the value type (F32 graphs)
+  static int batch_decode(dawn_solver_t s, void* out, int out_vt, int64_t ld, int nl, cudaStream_t stream) {
+    const int64_t n = s->g->n;
+    const int blocks = (int)std::min<int64_t>(148 * 8, (n + 31) / 32);
+    const bool dev = is_device_ptr(out);
+    const size_t es = out_vt == DAWN_F64 ? 8 : 4;
+    void* target = out;
+    if (!dev) {
+      if (!s->bout) CK(cudaMalloc(&s->bout, 8 * BL * (size_t)n));
+      target = s->bout;
+    }
+    const int64_t tld = dev ? ld : n;
+    if (out_vt == DAWN_F64)
+      dawn_batch_decode<V, double><<<blocks, 256, 0, stream>>>((const K*)s->bd, (uint32_t)n, (uint32_t)nl,
+                                                               (double*)target, (size_t)tld);
+    else
+      dawn_batch_decode<V, float><<<blocks, 256, 0, stream>>>((const K*)s->bd, (uint32_t)n, (uint32_t)nl,
+                                                              (float*)target, (size_t)tld);
+    CK(cudaGetLastError());
+    if (!dev)
+      CK(cudaMemcpy2DAsync(out, es * (size_t)ld, target, es * (size_t)n, es * (size_t)n, (size_t)nl,
+                           cudaMemcpyDeviceToHost, stream));
+    return DAWN_OK;
+  }
+
   static int alloc(dawn_solver_t s) {
     const int64_t n = s->g->n, m = s->g->m;
     const size_t ks = sizeof(K), es = sizeof(EI);
@@ -550,6 +677,17 @@ static void solver_free(dawn_solver_t s) {
   cudaFreeHost(s->st_host);
   cudaFree(s->dbuf);
   cudaFree(s->prof);
+  cudaFree(s->bd);
+  for (int i = 0; i < 4; ++i) cudaFree(s->bmask[i]);
+  cudaFree(s->bqnode);
+  cudaFree(s->bqmask);
+  cudaFree(s->bqoff);
+  cudaFree(s->bqbase);
+  cudaFree(s->bqkey);
+  cudaFree(s->btile);
+  cudaFree(s->bst);
+  cudaFreeHost(s->bst_host);
+  cudaFree(s->bout);
   delete s;
 }
 
@@ -580,6 +718,11 @@ extern "C" int dawn_solver_tune(dawn_solver_t s, const char* key, double value) 
     s->dense_edges_per_node = value;
     return DAWN_OK;
   }
+  if (!strcmp(key, "batch_min_sources")) {
+    if (!(value >= 0.0)) return fail(DAWN_EINVAL, "batch_min_sources must be >= 0");
+    s->batch_min_sources = value;
+    return DAWN_OK;
+  }
   return fail(DAWN_EINVAL, "unknown tuning key '%s'", key);
 }
 
@@ -602,6 +745,7 @@ static int do_begin(dawn_solver_t s, int64_t source, int algo, unsigned flags, c
   CK(cudaSetDevice(s->g->device));
   s->source = source;
   s->algo = algo;
+  s->last_batch = false;
   s->run_flags = flags & (s->flags | DAWN_F_NEGCHECK);
   if ((s->run_flags & DAWN_F_NEGCHECK) && !s->pred) s->run_flags &= ~DAWN_F_NEGCHECK;
   s->active = true;
@@ -695,15 +839,91 @@ extern "C" int dawn_solver_result(dawn_solver_t s, double* dist_out, int64_t* pr
 
 extern "C" int dawn_solver_round_profile(dawn_solver_t s, uint64_t* out, int64_t cap_rounds,
                                          int64_t* nrounds, void* stream) {
-  if (!s || !s->active) return fail(DAWN_EINVAL, "no solve has run on this solver");
+  if (!s || !(s->active || s->last_batch)) return fail(DAWN_EINVAL, "no solve has run on this solver");
   if (!s->prof) return fail(DAWN_EINVAL, "solver was created without DAWN_F_PROFILE");
   cudaStream_t st = (cudaStream_t)stream;
   CK(cudaSetDevice(s->g->device));
-  TRY(read_state(s, st));
-  const int64_t done = std::min<int64_t>((int64_t)s->st_host->round, (int64_t)s->prof_cap);
+  int64_t rounds_run = 0;
+  if (s->last_batch) {
+    BState b;
+    CK(cudaMemcpyAsync(&b, s->bst, sizeof(BState), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    rounds_run = (int64_t)b.rounds + 2;
+  } else {
+    TRY(read_state(s, st));
+    rounds_run = (int64_t)s->st_host->round;
+  }
+  const int64_t done = std::min<int64_t>(rounds_run, (int64_t)s->prof_cap);
   const int64_t k = std::min<int64_t>(done, cap_rounds);
   if (out && k > 0) CK(cudaMemcpy(out, s->prof, 32 * (size_t)k, cudaMemcpyDeviceToHost));
   if (nrounds) *nrounds = done;
+  return DAWN_OK;
+}
+
+static bool batch_ok(dawn_solver_t s, int algo, unsigned flags) {
+  return !s->g->has_negative && s->g->n >= 2 && !(flags & DAWN_F_PRED) && (algo == DAWN_GOVM || algo == DAWN_GSVM);
+}
+
+extern "C" int dawn_batch_supported(dawn_solver_t s, int algo, unsigned flags, int* out) {
+  if (!s || !out) return fail(DAWN_EINVAL, "NULL argument");
+  *out = batch_ok(s, algo, flags) ? 1 : 0;
+  return DAWN_OK;
+}
+
+static void fill_batch_stats(const BState& b, int nl, int64_t n, dawn_stats_t* o) {
+  for (int l = 0; l < nl; ++l) {
+    const int64_t lw = (int64_t)b.lastw[l];
+    o[l].outer_steps = std::min<int64_t>(std::max<int64_t>(lw + 1, 2), n);
+    o[l].relaxations = (int64_t)b.R[l];
+    o[l].writes = (int64_t)b.W[l];
+    o[l].first_discoveries = (int64_t)b.FD[l];
+    o[l].multi_written = (int64_t)b.MW[l];
+    o[l].negative_cycle = (((b.guard >> l) & 1u) || lw >= n) ? 1 : 0;
+    o[l].early_exit = 0;
+  }
+}
+
+extern "C" int dawn_mssp_batch(dawn_solver_t s, const int64_t* sources, int64_t k, int algo, unsigned flags,
+                               void* dist_out, int out_vtype, int64_t ld, dawn_stats_t* stats_out, void* stream) {
+  if (!s) return fail(DAWN_EINVAL, "solver is NULL");
+  if (k < 0 || (k > 0 && !sources)) return fail(DAWN_EINVAL, "bad sources");
+  for (int64_t i = 0; i < k; ++i) TRY(check_solve_args(s, sources[i], algo, flags & ~DAWN_F_PRED));
+  if (!batch_ok(s, algo, flags))
+    return fail(DAWN_EUNSUPPORTED, "batched solve needs non-negative weights, n >= 2 and no predecessors");
+  if (dist_out) {
+    if (out_vtype != DAWN_F64 && !(out_vtype == DAWN_F32 && s->g->vtype == DAWN_F32))
+      return fail(DAWN_EINVAL, "out_vtype must be DAWN_F64 (or DAWN_F32 for a float32 graph)");
+    if (ld < s->g->n) return fail(DAWN_EINVAL, "ld must be >= n");
+  }
+  if (k == 0) return DAWN_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  CK(cudaSetDevice(s->g->device));
+  const int64_t n = s->g->n;
+  const int64_t nb = (k + BL - 1) / BL;
+  if (stats_out && s->bst_host_cap < nb) {
+    CK(cudaStreamSynchronize(st));  // a previous asynchronous call may still write the old buffer
+    cudaFreeHost(s->bst_host);
+    s->bst_host = nullptr;
+    s->bst_host_cap = 0;
+    CK(cudaMallocHost(&s->bst_host, sizeof(BState) * nb));
+    s->bst_host_cap = nb;
+  }
+  const size_t es = out_vtype == DAWN_F64 ? 8 : 4;
+  const bool host_out = dist_out && !is_device_ptr(dist_out);
+  s->last_batch = true;
+  for (int64_t b = 0; b < nb; ++b) {
+    const int nl = (int)std::min<int64_t>(BL, k - b * BL);
+    TRY(DISPATCH(s->g, batch_run(s, sources + b * BL, nl, algo, st)));
+    if (dist_out)
+      TRY(DISPATCH(s->g, batch_decode(s, (char*)dist_out + (size_t)b * BL * ld * es, out_vtype, ld, nl, st)));
+    if (stats_out) CK(cudaMemcpyAsync(s->bst_host + b, s->bst, sizeof(BState), cudaMemcpyDeviceToHost, st));
+  }
+  if (stats_out || host_out) {
+    CK(cudaStreamSynchronize(st));
+    if (stats_out)
+      for (int64_t b = 0; b < nb; ++b)
+        fill_batch_stats(s->bst_host[b], (int)std::min<int64_t>(BL, k - b * BL), n, stats_out + b * BL);
+  }
   return DAWN_OK;
 }
 
@@ -712,6 +932,8 @@ extern "C" int dawn_mssp(dawn_solver_t s, const int64_t* sources, int64_t k, int
   if (!s) return fail(DAWN_EINVAL, "solver is NULL");
   if (k < 0 || (k > 0 && !sources)) return fail(DAWN_EINVAL, "bad sources");
   for (int64_t i = 0; i < k; ++i) TRY(check_solve_args(s, sources[i], algo, flags & ~DAWN_F_PRED));
+  if (k > 0 && (double)k >= s->batch_min_sources && batch_ok(s, algo, flags))
+    return dawn_mssp_batch(s, sources, k, algo, flags, dist_out, DAWN_F64, s->g->n, stats_out, stream);
   cudaStream_t st = (cudaStream_t)stream;
   CK(cudaSetDevice(s->g->device));
   DevState* hs = nullptr;

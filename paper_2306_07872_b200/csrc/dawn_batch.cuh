@@ -1,0 +1,585 @@
+// dawn_batch.cuh — batched multi-source weighted DAWN (K9 of SURVEY §7.2).
+//
+// Replaces the per-source loop of mssp / apsp (solver.py:426-495): up to 32
+// sources advance together, one per warp lane.  Distances are stored
+// node-major, bd[v][l] (l = source lane), so the 32 lanes of a warp that
+// relax one edge (u, v, w) read and update one contiguous 128-byte line
+// (4-byte values) — the edge's (col, w) is read once for all sources and
+// the dist gather is a single coalesced request instead of 32 random ones.
+//
+// Round r of the batch (each lane follows exactly the snapshot-Jacobi
+// semantics of the single-source kernel, so every per-source distance AND
+// counter equals a single-source solve — DESIGN.md §Batched multi-source):
+//
+//   B (build): a coalesced sweep over nmask[v] = lanes that lowered v in
+//      round r-1.  It clears nmask, does the write bookkeeping of round r-1
+//      (writes, first discoveries, nodes lowered in >= 2 rounds: per-lane
+//      counts via warp REDUX, no atomics), and lays the frontier of round r
+//      out as entries {node, lane mask, edge offset, row base} plus a
+//      32-lane snapshot of the row's distances (the value each lane relaxes
+//      with, as of the start of the round).  GOVM: lane mask = lanes that
+//      lowered the node (Alg. 2); GSVM: lanes where the node
+//      is finite and the lane is still running (solver.py:287-289).
+//   X (expand): warps stream WT-edge tiles of the frontier's virtual edge
+//      list (merge-path balanced, as the single-source kernel).  Per edge,
+//      each active lane forms cand = snap + w, reads its bd[v][lane]
+//      (one 128 B line for the warp) and, when cand < cur, issues a
+//      fire-and-forget red.min and the warp ORs the improved lanes into
+//      nmask[v] (red.or): the strict `>` relax of solver.py:298, :373.
+//
+// Only graphs without negative weights take this path (raw-bit keys, no
+// negative-cycle machinery); the host routes everything else to the
+// single-source kernel, one source at a time.
+#pragma once
+#include "dawn_kernels.cuh"
+
+namespace dawn {
+
+constexpr int BL = 32;    // sources per batch (warp lanes)
+constexpr int BWT = 128;  // virtual edges per warp tile
+
+struct BState {
+  unsigned long long res[2];   // packed frontier reservation (count << ebits | edges), by round parity
+  unsigned bar;                // grid barrier word (never reset)
+  unsigned wrote[2];           // lanes that lowered any node in the round with this parity
+  unsigned guard;              // lanes whose source guard fired (solver.py:299-303)
+  unsigned rounds;             // rounds executed (incl. seeding)
+  unsigned lastw[BL];          // per lane: last round that lowered a node (0 = none)
+  unsigned long long R[BL], W[BL], FD[BL], MW[BL];
+};
+
+template <class V, class EI>
+struct BParams {
+  using K = typename Val<V>::K;
+  uint32_t n;
+  uint32_t nlanes;                 // sources in this batch (<= 32)
+  const EI* row_ptr;
+  const uint2* e2;
+  const uint32_t* ecol;
+  const unsigned long long* ew;
+  K* bd;                           // [n][32] distance keys (raw bits)
+  uint32_t* nmask;                 // [n] lanes that lowered the node this round
+  uint32_t* w1;                    // [n] lanes that lowered it in >= 1 round
+  uint32_t* w2;                    // [n] ... in >= 2 rounds
+  uint32_t* smask;                 // [n] lanes whose source is the node (GSVM frontier)
+  uint32_t* qnode;
+  uint32_t* qmask;
+  EI* qoff;
+  EI* qbase;
+  K* qkey;                         // [cap][32] snapshot of the frontier rows
+  uint32_t* tile_row;
+  BState* st;
+  uint32_t src[BL];                // lane -> source node (0xFFFFFFFF = unused lane)
+  int ebits;
+  int algo;                        // 0 = GOVM, 1 = GSVM
+  unsigned long long* prof;        // optional per-round timeline, 4 words/round, or nullptr
+  unsigned prof_cap;
+};
+
+template <class V, class EI>
+struct __align__(16) BSmem {
+  unsigned long long scr64[NT / 32];
+  unsigned long long basepk;
+};
+
+template <class V> struct BEdge;
+template <> struct BEdge<float> {
+  template <class P, class EI> __device__ __forceinline__ static void load(const P& p, EI pos, uint32_t& c, uint32_t& w) {
+    uint2 x = ld_stream(p.e2 + pos); c = x.x; w = x.y;
+  }
+};
+template <> struct BEdge<int32_t> {
+  template <class P, class EI> __device__ __forceinline__ static void load(const P& p, EI pos, uint32_t& c, uint32_t& w) {
+    uint2 x = ld_stream(p.e2 + pos); c = x.x; w = x.y;
+  }
+};
+template <> struct BEdge<double> {
+  template <class P, class EI> __device__ __forceinline__ static void load(const P& p, EI pos, uint32_t& c, unsigned long long& w) {
+    c = ld_stream(p.ecol + pos); w = ld_stream(p.ew + pos);
+  }
+};
+template <> struct BEdge<int64_t> {
+  template <class P, class EI> __device__ __forceinline__ static void load(const P& p, EI pos, uint32_t& c, unsigned long long& w) {
+    c = ld_stream(p.ecol + pos); w = ld_stream(p.ew + pos);
+  }
+};
+
+template <class T>
+__device__ __forceinline__ T shfl_any(T v, int src) {
+  if constexpr (sizeof(T) == 8) {
+    const unsigned long long x = (unsigned long long)v;
+    unsigned lo = __shfl_sync(0xffffffffu, (unsigned)x, src);
+    unsigned hi = __shfl_sync(0xffffffffu, (unsigned)(x >> 32), src);
+    return (T)(((unsigned long long)hi << 32) | lo);
+  } else {
+    return (T)__shfl_sync(0xffffffffu, (unsigned)v, src);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// B phase: consume nmask (round r-1's writes), build round r's frontier
+// ---------------------------------------------------------------------------
+template <class V, class EI>
+__device__ void bphase_build(const BParams<V, EI>& P, uint32_t r, uint32_t active, BSmem<V, EI>& s,
+                             unsigned long long& accW, unsigned long long& accFD,
+                             unsigned long long& accMW, unsigned long long& accR) {
+  using K = typename Val<V>::K;
+  const uint32_t n = P.n;
+  const uint32_t nchunks = (n + TILE - 1) / TILE;
+  const uint32_t lane = threadIdx.x & 31;
+  const int eb = P.ebits;
+  const bool gsvm = P.algo == 1 && r >= 2;
+  for (uint32_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+    const uint32_t u0 = c * TILE + threadIdx.x * ITEMS;
+    const bool full = u0 + ITEMS <= n;
+    uint32_t M[ITEMS];
+    if (full) ldcg8<uint32_t>(P.nmask + u0, M);
+    else {
+#pragma unroll
+      for (int j = 0; j < ITEMS; ++j) M[j] = (u0 + j < n) ? ldcg(P.nmask + u0 + j) : 0u;
+    }
+    uint32_t anyM = 0;
+#pragma unroll
+    for (int j = 0; j < ITEMS; ++j) anyM |= M[j];
+    uint32_t W1[ITEMS];
+#pragma unroll
+    for (int j = 0; j < ITEMS; ++j) W1[j] = 0;
+    if (anyM || gsvm) {
+      if (full) ldcg8<uint32_t>(P.w1 + u0, W1);
+      else {
+#pragma unroll
+        for (int j = 0; j < ITEMS; ++j) W1[j] = (u0 + j < n) ? ldcg(P.w1 + u0 + j) : 0u;
+      }
+    }
+    if (r >= 2) {
+      // ---- write bookkeeping of round r-1 (the seeding round's frontier is not a write) ----
+      uint32_t FDm[ITEMS], MWm[ITEMS];
+#pragma unroll
+      for (int j = 0; j < ITEMS; ++j) { FDm[j] = 0; MWm[j] = 0; }
+      if (anyM) {
+        uint32_t W2[ITEMS];
+        if (full) ldcg8<uint32_t>(P.w2 + u0, W2);
+        else {
+#pragma unroll
+          for (int j = 0; j < ITEMS; ++j) W2[j] = (u0 + j < n) ? ldcg(P.w2 + u0 + j) : 0u;
+        }
+#pragma unroll
+        for (int j = 0; j < ITEMS; ++j) {
+          FDm[j] = M[j] & ~W1[j];
+          MWm[j] = M[j] & W1[j] & ~W2[j];
+          W2[j] |= M[j] & W1[j];
+          W1[j] |= M[j];
+        }
+        if (full) {
+          reinterpret_cast<uint4*>(P.w1 + u0)[0] = make_uint4(W1[0], W1[1], W1[2], W1[3]);
+          reinterpret_cast<uint4*>(P.w1 + u0)[1] = make_uint4(W1[4], W1[5], W1[6], W1[7]);
+          reinterpret_cast<uint4*>(P.w2 + u0)[0] = make_uint4(W2[0], W2[1], W2[2], W2[3]);
+          reinterpret_cast<uint4*>(P.w2 + u0)[1] = make_uint4(W2[4], W2[5], W2[6], W2[7]);
+          reinterpret_cast<uint4*>(P.nmask + u0)[0] = make_uint4(0, 0, 0, 0);
+          reinterpret_cast<uint4*>(P.nmask + u0)[1] = make_uint4(0, 0, 0, 0);
+        } else {
+#pragma unroll
+          for (int j = 0; j < ITEMS; ++j)
+            if (u0 + j < n) { P.w1[u0 + j] = W1[j]; P.w2[u0 + j] = W2[j]; P.nmask[u0 + j] = 0u; }
+        }
+      }
+      // per-lane counts: lane b sums bit b over the warp's nodes (one REDUX per bit)
+#pragma unroll 1
+      for (int j = 0; j < ITEMS; ++j) {
+        if (__any_sync(0xffffffffu, M[j] != 0u)) {
+#pragma unroll 4
+          for (int b = 0; b < BL; ++b) {
+            const uint32_t x = ((M[j] >> b) & 1u) | (((FDm[j] >> b) & 1u) << 10) | (((MWm[j] >> b) & 1u) << 20);
+            const uint32_t t = __reduce_add_sync(0xffffffffu, x);
+            if (lane == (uint32_t)b) {
+              accW += t & 1023u;
+              accFD += (t >> 10) & 1023u;
+              accMW += t >> 20;
+            }
+          }
+        }
+      }
+    } else if (anyM) {
+      if (full) {
+        reinterpret_cast<uint4*>(P.nmask + u0)[0] = make_uint4(0, 0, 0, 0);
+        reinterpret_cast<uint4*>(P.nmask + u0)[1] = make_uint4(0, 0, 0, 0);
+      } else {
+#pragma unroll
+        for (int j = 0; j < ITEMS; ++j)
+          if (u0 + j < n) P.nmask[u0 + j] = 0u;
+      }
+    }
+    // ---- frontier of round r ----
+    uint32_t F[ITEMS];
+    if (gsvm) {
+      uint32_t SM[ITEMS];
+      if (full) ldcg8<uint32_t>(P.smask + u0, SM);
+      else {
+#pragma unroll
+        for (int j = 0; j < ITEMS; ++j) SM[j] = (u0 + j < n) ? ldcg(P.smask + u0 + j) : 0u;
+      }
+#pragma unroll
+      for (int j = 0; j < ITEMS; ++j) F[j] = (W1[j] | SM[j]) & active;
+    } else {
+#pragma unroll
+      for (int j = 0; j < ITEMS; ++j) F[j] = M[j];
+    }
+    uint32_t anyF = 0;
+#pragma unroll
+    for (int j = 0; j < ITEMS; ++j) anyF |= F[j];
+    EI rp[ITEMS + 1];
+    unsigned sel = 0;
+    uint32_t mycnt = 0;
+    EI mydeg = 0;
+    if (anyF) {
+      if (full) {
+        ldg8<EI>(P.row_ptr + u0, *reinterpret_cast<EI(*)[ITEMS]>(rp));
+        rp[ITEMS] = __ldg(P.row_ptr + u0 + ITEMS);
+      } else {
+#pragma unroll
+        for (int j = 0; j < ITEMS; ++j) rp[j] = (u0 + j <= n) ? __ldg(P.row_ptr + u0 + j) : (EI)0;
+        rp[ITEMS] = (u0 + ITEMS <= n) ? __ldg(P.row_ptr + u0 + ITEMS) : (EI)0;
+      }
+#pragma unroll
+      for (int j = 0; j < ITEMS; ++j) {
+        if (F[j] && u0 + j < n && rp[j + 1] > rp[j]) {
+          sel |= 1u << j;
+          mycnt++;
+          mydeg += rp[j + 1] - rp[j];
+        }
+      }
+    }
+    const unsigned long long mine = ((unsigned long long)mycnt << eb) | (unsigned long long)mydeg;
+    unsigned long long tot;
+    const unsigned long long incl = block_incl_sum<unsigned long long>(mine, s.scr64, &tot);
+    if (threadIdx.x == 0 && tot != 0ull) s.basepk = atomicAdd(&P.st->res[r & 1], tot);
+    __syncthreads();
+    if (!__any_sync(0xffffffffu, sel != 0u)) continue;
+    // per-lane relaxations of round r: lane b sums the degrees of the warp's rows with bit b
+    {
+      unsigned long long le = 0;  // lane-edges (profile)
+#pragma unroll 1
+      for (int j = 0; j < ITEMS; ++j) {
+        const uint32_t fj = ((sel >> j) & 1u) ? F[j] : 0u;
+        if (__any_sync(0xffffffffu, fj != 0u)) {
+          const unsigned long long dj = fj ? (unsigned long long)(rp[j + 1] - rp[j]) : 0ull;
+          le += (unsigned long long)__popc(fj) * dj;
+          if (!__any_sync(0xffffffffu, dj >= (1ull << 26))) {  // warp sum < 2^31: one REDUX per bit
+#pragma unroll 4
+            for (int b = 0; b < BL; ++b) {
+              const uint32_t t = __reduce_add_sync(0xffffffffu, ((fj >> b) & 1u) ? (uint32_t)dj : 0u);
+              if (lane == (uint32_t)b) accR += t;
+            }
+          } else {
+#pragma unroll 1
+            for (int b = 0; b < BL; ++b) {
+              unsigned long long x = ((fj >> b) & 1u) ? dj : 0ull;
+              x = warp_sum_u64(x);
+              if (lane == (uint32_t)b) accR += x;
+            }
+          }
+        }
+      }
+      if (P.prof != nullptr && r < P.prof_cap) {
+        le = warp_sum_u64(le);
+        if (lane == 0 && le) atomicAdd(P.prof + 4 * r + 3, le);
+      }
+    }
+    if (!sel) continue;
+    // this thread's entries: metadata, tile marks and the 32-lane snapshot
+    // (one full 128/256-byte line per entry, vector loads all in flight)
+    const unsigned long long at = s.basepk + incl - mine;
+    uint32_t pos = (uint32_t)pk_count(at, eb);
+    EI off = (EI)pk_edges(at, eb);
+    constexpr int NV = BL * (int)sizeof(K) / 16;
+#pragma unroll
+    for (int j = 0; j < ITEMS; ++j) {
+      if ((sel >> j) & 1u) {
+        const uint32_t v = u0 + j;
+        const EI dg = rp[j + 1] - rp[j];
+        const uint4* srcl = reinterpret_cast<const uint4*>(P.bd + (size_t)v * BL);
+        uint4* dstl = reinterpret_cast<uint4*>(P.qkey + (size_t)pos * BL);
+        uint4 x[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) x[q] = __ldcg(srcl + q);
+        P.qnode[pos] = v;
+        P.qmask[pos] = F[j];
+        P.qoff[pos] = off;
+        P.qbase[pos] = rp[j] - off;
+        {
+          const EI t0 = (off + (EI)(BWT - 1)) / (EI)BWT;
+          const EI t1 = (off + dg - 1) / (EI)BWT;
+          for (EI tt = t0; tt <= t1; ++tt) P.tile_row[tt] = pos;
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) dstl[q] = x[q];
+#pragma unroll
+        for (int h = 8; h < NV; h += 8) {  // 8-byte keys: second half of the line
+#pragma unroll
+          for (int q = 0; q < 8; ++q) x[q] = __ldcg(srcl + h + q);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) dstl[h + q] = x[q];
+        }
+        pos++;
+        off += dg;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// X phase.  A thread owns LPT = 16 / sizeof(key) consecutive source lanes of
+// one edge (one 16-byte vector of the node's distance line), so TPE = 32/LPT
+// threads cover an edge and a warp relaxes EPW = LPT edges per step; the
+// (col, w) pairs and row lookups of 32 edges are loaded cooperatively first.
+// ---------------------------------------------------------------------------
+template <class V>
+struct BLanes {
+  using K = typename Val<V>::K;
+  static constexpr int LPT = 16 / (int)sizeof(K);
+  static constexpr int TPE = BL / LPT;
+  static constexpr int EPW = 32 / TPE;
+  static constexpr uint32_t LMASK = (1u << LPT) - 1u;
+};
+
+template <class K, int LPT>
+__device__ __forceinline__ void ld16_ca(const K* p, K (&o)[LPT]) {
+  const uint4 x = __ldca(reinterpret_cast<const uint4*>(p));
+  if constexpr (LPT == 4) {
+    o[0] = (K)x.x; o[1] = (K)x.y; o[2] = (K)x.z; o[3] = (K)x.w;
+  } else {
+    o[0] = (K)(((unsigned long long)x.y << 32) | x.x);
+    o[1] = (K)(((unsigned long long)x.w << 32) | x.z);
+  }
+}
+
+template <class V, class EI>
+__device__ void bphase_expand(const BParams<V, EI>& P, uint32_t r, const uint32_t (&msrc)[BLanes<V>::LPT],
+                              unsigned& guard, unsigned& wrote) {
+  using CD = Codec<V, true>;
+  using K = typename CD::K;
+  using WB = typename CD::WB;
+  constexpr int LPT = BLanes<V>::LPT, TPE = BLanes<V>::TPE, EPW = BLanes<V>::EPW;
+  constexpr uint32_t LMASK = BLanes<V>::LMASK;
+  constexpr int STEPS = 32 / EPW;  // warp steps per 32-edge chunk
+  constexpr int U = sizeof(K) == 4 ? 4 : 2;  // steps in flight
+  const unsigned long long pk = ldcg(&P.st->res[r & 1]);
+  const uint32_t cnt = (uint32_t)pk_count(pk, P.ebits);
+  const EI E = (EI)pk_edges(pk, P.ebits);
+  if (E == 0) return;
+  const EI T = (E + (EI)(BWT - 1)) / (EI)BWT;
+  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const uint32_t sub = lane % TPE, eg = lane / TPE;
+  const uint32_t lsh = sub * LPT;  // first source lane of this thread
+  const EI GW = (EI)gridDim.x * WPB;
+  for (EI t = (EI)blockIdx.x * WPB + wid; t < T; t += GW) {
+    const EI e0 = t * (EI)BWT;
+    const uint32_t len = (E - e0 < (EI)BWT) ? (uint32_t)(E - e0) : (uint32_t)BWT;
+    const uint32_t i0 = ldcg(P.tile_row + t);
+    const uint32_t il = (t + 1 < T) ? ldcg(P.tile_row + t + 1) : cnt - 1;
+    uint32_t ck = 0xFFFFFFFFu, cm = 0;  // this thread's current row: entry, its lanes' mask bits
+    K cs[LPT];                          // ... its lanes' snapshot values
+#pragma unroll
+    for (int i = 0; i < LPT; ++i) cs[i] = 0;
+    for (uint32_t c = 0; c < len; c += 32) {
+      const uint32_t ej = c + lane;
+      const EI e = e0 + (EI)ej;
+      // row of this lane's edge: the last entry k in [i0, il] with qoff[k] <= e
+      uint32_t lo = i0;
+      if (il > i0) {
+        uint32_t hi = il;
+        while (lo < hi) {
+          const uint32_t mid = (lo + hi + 1) >> 1;
+          if (__ldca(P.qoff + mid) <= e) lo = mid; else hi = mid - 1;
+        }
+      }
+      uint32_t col = 0;
+      WB w = 0;
+      if (ej < len) BEdge<V>::load(P, __ldca(P.qbase + lo) + e, col, w);
+      const uint32_t nj = (len - c < 32u) ? len - c : 32u;
+      for (int q0 = 0; q0 < STEPS; q0 += U) {
+        if ((uint32_t)(q0 * EPW) >= nj) break;  // warp-uniform
+        K cand[U][LPT], cur[U][LPT];
+        uint32_t vq[U], am[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const uint32_t j = (uint32_t)((q0 + u) * EPW) + eg;
+          vq[u] = __shfl_sync(0xffffffffu, col, j & 31);
+          const uint32_t kq = __shfl_sync(0xffffffffu, lo, j & 31);
+          const WB wq = shfl_any<WB>(w, j & 31);
+          const bool valid = j < nj;
+          if (valid && kq != ck) {
+            ck = kq;
+            cm = (__ldca(P.qmask + kq) >> lsh) & LMASK;
+            if (cm) ld16_ca<K, LPT>(P.qkey + (size_t)kq * BL + lsh, cs);
+          }
+          uint32_t a = valid ? cm : 0u;
+#pragma unroll
+          for (int i = 0; i < LPT; ++i) {
+            cand[u][i] = CD::relax(CD::dec(cs[i]), wq);
+            if (!CD::usable(cand[u][i])) a &= ~(1u << i);
+          }
+          am[u] = a;
+          if (a) ld16_ca<K, LPT>(P.bd + (size_t)vq[u] * BL + lsh, cur[u]);
+          else {
+#pragma unroll
+            for (int i = 0; i < LPT; ++i) cur[u][i] = 0;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          uint32_t imp = 0;
+#pragma unroll
+          for (int i = 0; i < LPT; ++i) {
+            if (((am[u] >> i) & 1u) && cand[u][i] < cur[u][i]) {
+              if (vq[u] == msrc[i]) guard |= 1u << (lsh + i);  // source guard (solver.py:299-303)
+              else imp |= 1u << i;
+            }
+          }
+          if (imp) {
+#pragma unroll
+            for (int i = 0; i < LPT; ++i)
+              if ((imp >> i) & 1u) atomicMin(P.bd + (size_t)vq[u] * BL + lsh + i, cand[u][i]);
+          }
+          uint32_t bits = imp << lsh;
+#pragma unroll
+          for (int d = 1; d < TPE; d <<= 1) bits |= __shfl_xor_sync(0xffffffffu, bits, d);
+          if (sub == 0 && bits) atomicOr(P.nmask + vq[u], bits);
+          wrote |= bits;
+        }
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// the persistent batched kernel
+// ---------------------------------------------------------------------------
+template <class V, class EI>
+__global__ void __launch_bounds__(NT, DAWN_MIN_BLOCKS) dawn_batch_persistent(BParams<V, EI> P) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  BSmem<V, EI>& s = *reinterpret_cast<BSmem<V, EI>*>(smem_raw);
+  BState* st = P.st;
+  const uint32_t lane = threadIdx.x & 31;
+  const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
+  constexpr int LPT = BLanes<V>::LPT;
+  uint32_t msrc[LPT];  // sources of this thread's lanes in the X phase
+#pragma unroll
+  for (int i = 0; i < LPT; ++i) msrc[i] = P.src[(lane % BLanes<V>::TPE) * LPT + i];
+  unsigned long long accW = 0, accFD = 0, accMW = 0, accR = 0;
+  unsigned guard = 0;
+  uint32_t lastw = 0;  // this lane's last writing round (identical in every thread of the lane)
+  const uint32_t valid = __ballot_sync(0xffffffffu, lane < P.nlanes);
+  uint32_t active = valid;
+  uint32_t r = 1;
+  // Round r = B(r) [builds into res[r&1]] | barrier | X(r) [ORs its writers into
+  // wrote[r&1]] | barrier.  Double-buffered by parity, so every reset happens
+  // a full barrier after the last read of the slot and before its next write.
+  for (;; ++r) {
+    if (r >= 2) {
+      // ---- round r-1's writers; termination (solver.py:284-285, :356-358, :388-395) ----
+      const unsigned wr = ldcg(&st->wrote[(r - 1) & 1]);
+      if ((wr >> lane) & 1u) lastw = r - 1;
+      if (r >= 3) active &= wr;  // a lane runs round r iff it wrote in r-1 (round 2 always runs)
+      if (r >= 3 && wr == 0u) break;
+      if (r - 1 >= P.n) break;
+    }
+    // ---- B phase ----
+    const bool prof = leader && P.prof != nullptr && r < P.prof_cap;
+    if (prof) P.prof[4 * r + 0] = globaltimer();
+    if (leader) st->res[(r + 1) & 1] = 0ull;  // last read by X(r-1), next written by B(r+1)
+    bphase_build<V, EI>(P, r, active, s, accW, accFD, accMW, accR);
+    grid_sync(&st->bar);
+    // ---- X phase ----
+    if (prof) {
+      P.prof[4 * r + 1] = globaltimer();
+      P.prof[4 * r + 2] = ldcg(&st->res[r & 1]);
+    }
+    if (leader) st->wrote[(r + 1) & 1] = 0u;  // last read at the top of round r, next written by X(r+1)
+    unsigned wrote = 0;
+    bphase_expand<V, EI>(P, r, msrc, guard, wrote);
+    wrote = __reduce_or_sync(0xffffffffu, wrote);
+    if (lane == 0 && wrote) atomicOr(&st->wrote[r & 1], wrote);
+    grid_sync(&st->bar);
+  }
+  // ---- per-lane results ----
+  if (leader) st->rounds = r - 1;
+  if (leader && P.prof != nullptr && r < P.prof_cap) P.prof[4 * r + 0] = globaltimer();
+  guard = __reduce_or_sync(0xffffffffu, guard);
+  if (lane == 0 && guard) atomicOr(&st->guard, guard);
+  // block-level reduction of the per-lane counters, then one atomic per lane per CTA
+  __shared__ unsigned long long red[NT / 32][BL][4];
+  const uint32_t wid = threadIdx.x >> 5;
+  red[wid][lane][0] = accR;
+  red[wid][lane][1] = accW;
+  red[wid][lane][2] = accFD;
+  red[wid][lane][3] = accMW;
+  __syncthreads();
+  if (threadIdx.x < BL * 4) {
+    const uint32_t l = threadIdx.x >> 2, f = threadIdx.x & 3;
+    unsigned long long sum = 0;
+#pragma unroll
+    for (int w = 0; w < NT / 32; ++w) sum += red[w][l][f];
+    if (sum) {
+      unsigned long long* dst = f == 0 ? st->R : f == 1 ? st->W : f == 2 ? st->FD : st->MW;
+      atomicAdd(dst + l, sum);
+    }
+  }
+  if (blockIdx.x == 0 && wid == 0) st->lastw[lane] = lastw;
+}
+
+// batch init: sources' own distance 0, their bit in nmask (the seeding
+// frontier) and smask; everything else was memset by the host.
+template <class V, class EI>
+__global__ void dawn_batch_init(BParams<V, EI> P) {
+  const uint32_t l = threadIdx.x;
+  if (l < P.nlanes) {
+    const uint32_t s = P.src[l];
+    P.bd[(size_t)s * BL + l] = Codec<V, true>::enc((V)0);
+    atomicOr(P.nmask + s, 1u << l);
+    atomicOr(P.smask + s, 1u << l);
+  }
+  if (l == 0) {
+    BState* st = P.st;
+    st->res[0] = st->res[1] = 0ull;
+    st->wrote[0] = st->wrote[1] = 0u;
+    st->guard = 0u;
+    st->rounds = 0u;
+  }
+  if (l < BL) {
+    P.st->lastw[l] = 0u;
+    P.st->R[l] = P.st->W[l] = P.st->FD[l] = P.st->MW[l] = 0ull;
+  }
+}
+
+// bd[n][32] -> out[l][n] for l < nlanes (row-major source x node), via a
+// 32x32 shared-memory transpose.  OUT = double (reference DistanceVector)
+// or the value type itself (device-resident tiles).
+template <class V, class OUT>
+__global__ void dawn_batch_decode(const typename Val<V>::K* __restrict__ bd, uint32_t n, uint32_t nlanes,
+                                  OUT* __restrict__ out, size_t ld) {
+  __shared__ OUT tile[32][33];
+  const uint32_t tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8 threads
+  for (uint32_t v0 = blockIdx.x * 32; v0 < n; v0 += gridDim.x * 32) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t v = v0 + ty + 8 * k;
+      OUT x = 0;
+      if (v < n) {
+        const typename Val<V>::K key = bd[(size_t)v * BL + tx];
+        x = (OUT)Codec<V, true>::to_f64(key);
+      }
+      tile[ty + 8 * k][tx] = x;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t l = ty + 8 * k;
+      const uint32_t v = v0 + tx;
+      if (l < nlanes && v < n) out[(size_t)l * ld + v] = tile[tx][l];
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace dawn
