@@ -523,7 +523,7 @@ struct Impl {
     const size_t sm = sizeof(BSmem<V, EI>);
     CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     {
-      const double need_kb = DAWN_MIN_BLOCKS * ((double)(sm + 8 * 1024) / 1024.0 + 1.0);
+      const double need_kb = DAWN_BATCH_MIN_BLOCKS * ((double)(sm + 8 * 1024) / 1024.0 + 1.0);
       const int pct = std::min(100, (int)std::ceil(100.0 * need_kb / 228.0));
       CK(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
     }

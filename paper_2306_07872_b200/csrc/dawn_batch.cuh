@@ -35,8 +35,12 @@
 
 namespace dawn {
 
+#ifndef DAWN_BATCH_MIN_BLOCKS
+#define DAWN_BATCH_MIN_BLOCKS 2  // resident CTAs per SM the batched kernel's registers are sized for
+#endif
+
 constexpr int BL = 32;    // sources per batch (warp lanes)
-constexpr int BWT = 128;  // virtual edges per warp tile
+constexpr int BWT = 32;   // virtual edges per warp tile (<= 32 rows per tile)
 
 struct BState {
   unsigned long long res[2];   // packed frontier reservation (count << ebits | edges), by round parity
@@ -122,7 +126,7 @@ __device__ __forceinline__ T shfl_any(T v, int src) {
 template <class V, class EI>
 __device__ void bphase_build(const BParams<V, EI>& P, uint32_t r, uint32_t active, BSmem<V, EI>& s,
                              unsigned long long& accW, unsigned long long& accFD,
-                             unsigned long long& accMW, unsigned long long& accR) {
+                             unsigned long long& accMW) {
   using K = typename Val<V>::K;
   const uint32_t n = P.n;
   const uint32_t nchunks = (n + TILE - 1) / TILE;
@@ -255,35 +259,13 @@ __device__ void bphase_build(const BParams<V, EI>& P, uint32_t r, uint32_t activ
     if (threadIdx.x == 0 && tot != 0ull) s.basepk = atomicAdd(&P.st->res[r & 1], tot);
     __syncthreads();
     if (!__any_sync(0xffffffffu, sel != 0u)) continue;
-    // per-lane relaxations of round r: lane b sums the degrees of the warp's rows with bit b
-    {
-      unsigned long long le = 0;  // lane-edges (profile)
-#pragma unroll 1
-      for (int j = 0; j < ITEMS; ++j) {
-        const uint32_t fj = ((sel >> j) & 1u) ? F[j] : 0u;
-        if (__any_sync(0xffffffffu, fj != 0u)) {
-          const unsigned long long dj = fj ? (unsigned long long)(rp[j + 1] - rp[j]) : 0ull;
-          le += (unsigned long long)__popc(fj) * dj;
-          if (!__any_sync(0xffffffffu, dj >= (1ull << 26))) {  // warp sum < 2^31: one REDUX per bit
-#pragma unroll 4
-            for (int b = 0; b < BL; ++b) {
-              const uint32_t t = __reduce_add_sync(0xffffffffu, ((fj >> b) & 1u) ? (uint32_t)dj : 0u);
-              if (lane == (uint32_t)b) accR += t;
-            }
-          } else {
-#pragma unroll 1
-            for (int b = 0; b < BL; ++b) {
-              unsigned long long x = ((fj >> b) & 1u) ? dj : 0ull;
-              x = warp_sum_u64(x);
-              if (lane == (uint32_t)b) accR += x;
-            }
-          }
-        }
-      }
-      if (P.prof != nullptr && r < P.prof_cap) {
-        le = warp_sum_u64(le);
-        if (lane == 0 && le) atomicAdd(P.prof + 4 * r + 3, le);
-      }
+    if (P.prof != nullptr && r < P.prof_cap) {  // lane-edges of round r (profile only)
+      unsigned long long le = 0;
+#pragma unroll
+      for (int j = 0; j < ITEMS; ++j)
+        if ((sel >> j) & 1u) le += (unsigned long long)__popc(F[j]) * (unsigned long long)(rp[j + 1] - rp[j]);
+      le = warp_sum_u64(le);
+      if (lane == 0 && le) atomicAdd(P.prof + 4 * r + 3, le);
     }
     if (!sel) continue;
     // this thread's entries: metadata, tile marks and the 32-lane snapshot
@@ -353,16 +335,76 @@ __device__ __forceinline__ void ld16_ca(const K* p, K (&o)[LPT]) {
   }
 }
 
+// One 32-edge tile of the frontier's virtual edge list as a warp sees it:
+// lane j holds edge j (column, weight, row index relative to i0) and lane k
+// holds row i0+k's lane mask (a tile spans at most 32 rows: its first row
+// owns edge 0, every other row starts inside it).
+template <class WB>
+struct BTile {
+  uint32_t i0;     // first entry
+  uint32_t len;    // edges in the tile (0 = no tile)
+  uint32_t col;    // lane j: column of edge j
+  WB w;            // lane j: weight bits of edge j
+  uint32_t kr;     // lane j: row of edge j, relative to i0
+  uint32_t rmask;  // lane k: lane mask of row i0+k
+};
+
+template <class V, class EI>
+struct BRows {        // row metadata of a tile in flight
+  uint32_t i0, il;
+  EI off, base;       // lane k: row i0+k
+  uint32_t rmask;
+};
+
+template <class V, class EI>
+__device__ __forceinline__ void brows_load(const BParams<V, EI>& P, EI t, EI T, uint32_t cnt, uint32_t lane,
+                                           BRows<V, EI>& R) {
+  R.i0 = __ldca(P.tile_row + t);
+  R.il = (t + 1 < T) ? __ldca(P.tile_row + t + 1) : cnt - 1;
+  R.off = 0;
+  R.base = 0;
+  R.rmask = 0;
+  if (lane <= R.il - R.i0) {
+    R.off = __ldca(P.qoff + R.i0 + lane);
+    R.base = __ldca(P.qbase + R.i0 + lane);
+    R.rmask = __ldca(P.qmask + R.i0 + lane);
+  }
+}
+
+// row of every edge (row-start bits + popc), then the edge loads
+template <class V, class EI>
+__device__ __forceinline__ void btile_issue(const BParams<V, EI>& P, EI t, EI E, uint32_t lane,
+                                            const BRows<V, EI>& R, BTile<typename Val<V>::K>& X) {
+  const EI e0 = t * (EI)BWT;
+  X.len = (E - e0 < (EI)BWT) ? (uint32_t)(E - e0) : (uint32_t)BWT;
+  X.i0 = R.i0;
+  X.rmask = R.rmask;
+  const uint32_t nrows = R.il - R.i0 + 1;
+  const uint32_t rst = (lane < nrows && R.off >= e0 && R.off - e0 < (EI)32) ? (uint32_t)(R.off - e0) : 32u;
+  const uint32_t B = __reduce_or_sync(0xffffffffu, rst < 32u ? (1u << rst) : 0u);
+  const uint32_t start0 = B & 1u;  // row i0 starts exactly at the tile
+  X.kr = (uint32_t)__popc(B & (0xFFFFFFFFu >> (31 - lane))) - start0;
+  const EI base = shfl_any<EI>(R.base, (int)X.kr);
+  X.col = 0;
+  X.w = 0;
+  if (lane < X.len) BEdge<V>::load(P, base + e0 + (EI)lane, X.col, X.w);
+}
+
 template <class V, class EI>
 __device__ void bphase_expand(const BParams<V, EI>& P, uint32_t r, const uint32_t (&msrc)[BLanes<V>::LPT],
-                              unsigned& guard, unsigned& wrote) {
+                              unsigned& guard, unsigned& wrote, unsigned long long (&accR)[BLanes<V>::LPT]) {
   using CD = Codec<V, true>;
   using K = typename CD::K;
   using WB = typename CD::WB;
   constexpr int LPT = BLanes<V>::LPT, TPE = BLanes<V>::TPE, EPW = BLanes<V>::EPW;
   constexpr uint32_t LMASK = BLanes<V>::LMASK;
-  constexpr int STEPS = 32 / EPW;  // warp steps per 32-edge chunk
-  constexpr int U = sizeof(K) == 4 ? 4 : 2;  // steps in flight
+  constexpr int STEPS = 32 / EPW;               // warp steps per tile
+  constexpr int U = sizeof(K) == 4 ? 4 : 2;     // steps in flight
+  // a candidate is usable iff it is below +inf: clamp the current value there,
+  // so `cand < min(cur, +inf)` is the reference's `alpha[idx] > cand` with an
+  // infinite candidate never written (solver.py:298, :373)
+  constexpr K CAP = std::is_same<V, float>::value ? (K)0x7F800000u
+                  : std::is_same<V, double>::value ? (K)0x7FF0000000000000ull : CD::INF;
   const unsigned long long pk = ldcg(&P.st->res[r & 1]);
   const uint32_t cnt = (uint32_t)pk_count(pk, P.ebits);
   const EI E = (EI)pk_edges(pk, P.ebits);
@@ -372,82 +414,98 @@ __device__ void bphase_expand(const BParams<V, EI>& P, uint32_t r, const uint32_
   const uint32_t sub = lane % TPE, eg = lane / TPE;
   const uint32_t lsh = sub * LPT;  // first source lane of this thread
   const EI GW = (EI)gridDim.x * WPB;
-  for (EI t = (EI)blockIdx.x * WPB + wid; t < T; t += GW) {
-    const EI e0 = t * (EI)BWT;
-    const uint32_t len = (E - e0 < (EI)BWT) ? (uint32_t)(E - e0) : (uint32_t)BWT;
-    const uint32_t i0 = ldcg(P.tile_row + t);
-    const uint32_t il = (t + 1 < T) ? ldcg(P.tile_row + t + 1) : cnt - 1;
-    uint32_t ck = 0xFFFFFFFFu, cm = 0;  // this thread's current row: entry, its lanes' mask bits
-    K cs[LPT];                          // ... its lanes' snapshot values
+  EI t = (EI)blockIdx.x * WPB + wid;
+  if (t >= T) return;  // warp-uniform
+  // software pipeline (depth 2): edges of tile t and t+GW in flight, rows of
+  // t+2GW in flight, while tile t's distance lines are gathered and relaxed
+  BTile<WB> A, Bt;
+  BRows<V, EI> Rn;
+  {
+    BRows<V, EI> R0;
+    brows_load<V, EI>(P, t, T, cnt, lane, R0);
+    btile_issue<V, EI>(P, t, E, lane, R0, A);
+  }
+  Bt.len = 0;
+  if (t + GW < T) {
+    BRows<V, EI> R1;
+    brows_load<V, EI>(P, t + GW, T, cnt, lane, R1);
+    btile_issue<V, EI>(P, t + GW, E, lane, R1, Bt);
+  }
+  bool have_rn = t + 2 * GW < T;
+  if (have_rn) brows_load<V, EI>(P, t + 2 * GW, T, cnt, lane, Rn);
+  // relaxations (solver.py:297, :372) of this thread's lanes: LPT 8/16-bit
+  // counters packed in one register (a thread sees STEPS <= 16 edges per tile),
+  // flushed into accR after every tile
+  constexpr uint32_t SPREAD = LPT == 4 ? 0x204081u : 0x8001u;     // bit i -> field i
+  constexpr uint32_t FMASK = LPT == 4 ? 0x01010101u : 0x00010001u;
+  constexpr int FBITS = LPT == 4 ? 8 : 16;
+  for (;;) {
+    // ---- relax tile A ----
+    uint32_t ck = 0xFFFFFFFFu;  // this thread's current row (relative to A.i0)
+    K cs[LPT];
 #pragma unroll
     for (int i = 0; i < LPT; ++i) cs[i] = 0;
-    for (uint32_t c = 0; c < len; c += 32) {
-      const uint32_t ej = c + lane;
-      const EI e = e0 + (EI)ej;
-      // row of this lane's edge: the last entry k in [i0, il] with qoff[k] <= e
-      uint32_t lo = i0;
-      if (il > i0) {
-        uint32_t hi = il;
-        while (lo < hi) {
-          const uint32_t mid = (lo + hi + 1) >> 1;
-          if (__ldca(P.qoff + mid) <= e) lo = mid; else hi = mid - 1;
+    uint32_t rcp = 0;
+#pragma unroll 1
+    for (int q0 = 0; q0 < STEPS; q0 += U) {
+      if ((uint32_t)(q0 * EPW) >= A.len) break;  // warp-uniform
+      K cand[U][LPT], cur[U][LPT];
+      uint32_t vq[U], am[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t j = (uint32_t)((q0 + u) * EPW) + eg;
+        vq[u] = __shfl_sync(0xffffffffu, A.col, j & 31);
+        const uint32_t kq = __shfl_sync(0xffffffffu, A.kr, j & 31);
+        const WB wq = shfl_any<WB>(A.w, j & 31);
+        const uint32_t mq = __shfl_sync(0xffffffffu, A.rmask, kq & 31);
+        const uint32_t a = (j < A.len) ? ((mq >> lsh) & LMASK) : 0u;
+        if (kq != ck) {  // the row's snapshot (L1)
+          ck = kq;
+          ld16_ca<K, LPT>(P.qkey + (size_t)(A.i0 + kq) * BL + lsh, cs);
         }
+#pragma unroll
+        for (int i = 0; i < LPT; ++i) cand[u][i] = CD::relax(CD::dec(cs[i]), wq);
+        rcp += (a * SPREAD) & FMASK;
+        am[u] = a;
+        // inactive threads re-read the tile's first line (an L1 hit) instead of branching
+        ld16_ca<K, LPT>(P.bd + (size_t)(a ? vq[u] : vq[0]) * BL + lsh, cur[u]);
       }
-      uint32_t col = 0;
-      WB w = 0;
-      if (ej < len) BEdge<V>::load(P, __ldca(P.qbase + lo) + e, col, w);
-      const uint32_t nj = (len - c < 32u) ? len - c : 32u;
-      for (int q0 = 0; q0 < STEPS; q0 += U) {
-        if ((uint32_t)(q0 * EPW) >= nj) break;  // warp-uniform
-        K cand[U][LPT], cur[U][LPT];
-        uint32_t vq[U], am[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const uint32_t j = (uint32_t)((q0 + u) * EPW) + eg;
-          vq[u] = __shfl_sync(0xffffffffu, col, j & 31);
-          const uint32_t kq = __shfl_sync(0xffffffffu, lo, j & 31);
-          const WB wq = shfl_any<WB>(w, j & 31);
-          const bool valid = j < nj;
-          if (valid && kq != ck) {
-            ck = kq;
-            cm = (__ldca(P.qmask + kq) >> lsh) & LMASK;
-            if (cm) ld16_ca<K, LPT>(P.qkey + (size_t)kq * BL + lsh, cs);
-          }
-          uint32_t a = valid ? cm : 0u;
+      for (int u = 0; u < U; ++u) {
+        uint32_t imp = 0;
 #pragma unroll
-          for (int i = 0; i < LPT; ++i) {
-            cand[u][i] = CD::relax(CD::dec(cs[i]), wq);
-            if (!CD::usable(cand[u][i])) a &= ~(1u << i);
-          }
-          am[u] = a;
-          if (a) ld16_ca<K, LPT>(P.bd + (size_t)vq[u] * BL + lsh, cur[u]);
-          else {
-#pragma unroll
-            for (int i = 0; i < LPT; ++i) cur[u][i] = 0;
-          }
+        for (int i = 0; i < LPT; ++i) {
+          const K cc = cur[u][i] < CAP ? cur[u][i] : CAP;
+          imp |= (((am[u] >> i) & 1u) && cand[u][i] < cc) ? (1u << i) : 0u;
         }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          uint32_t imp = 0;
+        if (imp) {
 #pragma unroll
           for (int i = 0; i < LPT; ++i) {
-            if (((am[u] >> i) & 1u) && cand[u][i] < cur[u][i]) {
-              if (vq[u] == msrc[i]) guard |= 1u << (lsh + i);  // source guard (solver.py:299-303)
-              else imp |= 1u << i;
+            if ((imp >> i) & 1u) {
+              if (vq[u] == msrc[i]) {  // source guard (solver.py:299-303)
+                guard |= 1u << (lsh + i);
+                imp &= ~(1u << i);
+              } else {
+                atomicMin(P.bd + (size_t)vq[u] * BL + lsh + i, cand[u][i]);
+              }
             }
           }
-          if (imp) {
-#pragma unroll
-            for (int i = 0; i < LPT; ++i)
-              if ((imp >> i) & 1u) atomicMin(P.bd + (size_t)vq[u] * BL + lsh + i, cand[u][i]);
-          }
-          uint32_t bits = imp << lsh;
-#pragma unroll
-          for (int d = 1; d < TPE; d <<= 1) bits |= __shfl_xor_sync(0xffffffffu, bits, d);
-          if (sub == 0 && bits) atomicOr(P.nmask + vq[u], bits);
-          wrote |= bits;
+          if (imp) atomicOr(P.nmask + vq[u], imp << lsh);
+          wrote |= imp << lsh;
         }
       }
+    }
+#pragma unroll
+    for (int i = 0; i < LPT; ++i) accR[i] += (rcp >> (FBITS * i)) & ((1u << FBITS) - 1u);
+    // ---- advance the pipeline ----
+    if (Bt.len == 0) break;  // warp-uniform: no next tile
+    t += GW;
+    A = Bt;
+    Bt.len = 0;
+    if (have_rn) {
+      btile_issue<V, EI>(P, t + GW, E, lane, Rn, Bt);
+      have_rn = t + 2 * GW < T;
+      if (have_rn) brows_load<V, EI>(P, t + 2 * GW, T, cnt, lane, Rn);
     }
   }
 }
@@ -456,7 +514,7 @@ __device__ void bphase_expand(const BParams<V, EI>& P, uint32_t r, const uint32_
 // the persistent batched kernel
 // ---------------------------------------------------------------------------
 template <class V, class EI>
-__global__ void __launch_bounds__(NT, DAWN_MIN_BLOCKS) dawn_batch_persistent(BParams<V, EI> P) {
+__global__ void __launch_bounds__(NT, DAWN_BATCH_MIN_BLOCKS) dawn_batch_persistent(BParams<V, EI> P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   BSmem<V, EI>& s = *reinterpret_cast<BSmem<V, EI>*>(smem_raw);
   BState* st = P.st;
@@ -466,7 +524,10 @@ __global__ void __launch_bounds__(NT, DAWN_MIN_BLOCKS) dawn_batch_persistent(BPa
   uint32_t msrc[LPT];  // sources of this thread's lanes in the X phase
 #pragma unroll
   for (int i = 0; i < LPT; ++i) msrc[i] = P.src[(lane % BLanes<V>::TPE) * LPT + i];
-  unsigned long long accW = 0, accFD = 0, accMW = 0, accR = 0;
+  unsigned long long accW = 0, accFD = 0, accMW = 0;
+  unsigned long long accR[BLanes<V>::LPT];  // relaxations of this thread's X-phase lanes
+#pragma unroll
+  for (int i = 0; i < BLanes<V>::LPT; ++i) accR[i] = 0;
   unsigned guard = 0;
   uint32_t lastw = 0;  // this lane's last writing round (identical in every thread of the lane)
   const uint32_t valid = __ballot_sync(0xffffffffu, lane < P.nlanes);
@@ -488,7 +549,7 @@ __global__ void __launch_bounds__(NT, DAWN_MIN_BLOCKS) dawn_batch_persistent(BPa
     const bool prof = leader && P.prof != nullptr && r < P.prof_cap;
     if (prof) P.prof[4 * r + 0] = globaltimer();
     if (leader) st->res[(r + 1) & 1] = 0ull;  // last read by X(r-1), next written by B(r+1)
-    bphase_build<V, EI>(P, r, active, s, accW, accFD, accMW, accR);
+    bphase_build<V, EI>(P, r, active, s, accW, accFD, accMW);
     grid_sync(&st->bar);
     // ---- X phase ----
     if (prof) {
@@ -497,7 +558,7 @@ __global__ void __launch_bounds__(NT, DAWN_MIN_BLOCKS) dawn_batch_persistent(BPa
     }
     if (leader) st->wrote[(r + 1) & 1] = 0u;  // last read at the top of round r, next written by X(r+1)
     unsigned wrote = 0;
-    bphase_expand<V, EI>(P, r, msrc, guard, wrote);
+    bphase_expand<V, EI>(P, r, msrc, guard, wrote, accR);
     wrote = __reduce_or_sync(0xffffffffu, wrote);
     if (lane == 0 && wrote) atomicOr(&st->wrote[r & 1], wrote);
     grid_sync(&st->bar);
@@ -510,7 +571,20 @@ __global__ void __launch_bounds__(NT, DAWN_MIN_BLOCKS) dawn_batch_persistent(BPa
   // block-level reduction of the per-lane counters, then one atomic per lane per CTA
   __shared__ unsigned long long red[NT / 32][BL][4];
   const uint32_t wid = threadIdx.x >> 5;
-  red[wid][lane][0] = accR;
+  // R: lanes with the same sub own the same source lanes; fold them, then the
+  // eg == 0 thread of each sub writes its LPT lanes
+  {
+    constexpr int TPE = BLanes<V>::TPE;
+#pragma unroll
+    for (int i = 0; i < BLanes<V>::LPT; ++i) {
+#pragma unroll
+      for (int d = TPE; d < 32; d <<= 1) accR[i] += __shfl_xor_sync(0xffffffffu, accR[i], d);
+    }
+    if (lane < (uint32_t)TPE) {
+#pragma unroll
+      for (int i = 0; i < BLanes<V>::LPT; ++i) red[wid][lane * BLanes<V>::LPT + i][0] = accR[i];
+    }
+  }
   red[wid][lane][1] = accW;
   red[wid][lane][2] = accFD;
   red[wid][lane][3] = accMW;
