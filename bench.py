@@ -46,6 +46,9 @@ def parse():
     ap.add_argument("--source", type=int, default=SOURCE)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=120.0, help="seconds for the reference arm's timed steps")
+    ap.add_argument("--no-apsp", action="store_true", help="skip the config-3 multi-source leg")
+    ap.add_argument("--apsp-sources", type=int, default=8192)
+    ap.add_argument("--apsp-scale", type=int, default=20)
     return ap.parse_args()
 
 
@@ -228,6 +231,77 @@ def reference_arm(args):
 
 
 # ---------------------------------------------------------------------------
+# config 3: multi-source APSP, sources sharded over the ranks
+# ---------------------------------------------------------------------------
+def run_apsp(args, rank, world, local):
+    """8192 sources on RMAT-20 ef16 (float32 weights), drawn as SURVEY §8(d)
+    says (default_rng(5) over vertices with out-degree >= 1, ascending).  The
+    timed window runs from the first launch to every float32 result row being
+    resident in rank 0's [k][n] tile (max over ranks)."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2306_07872_b200 import multisource as MS
+    from paper_2306_07872_b200.devgen import rmat_device_graph
+
+    dev = torch.device("cuda", local)
+    dg, _, deg = rmat_device_graph(args.apsp_scale, 16, weights="f32", precision="fp32", device=local)
+    degh = deg.cpu().numpy()
+    rng = np.random.default_rng(5)
+    cand = np.flatnonzero(degh > 0)
+    k = min(args.apsp_sources, cand.size)
+    src = sorted(int(x) for x in rng.choice(cand, size=k, replace=False))
+    tile = torch.empty((k, dg.n), dtype=torch.float32, device=dev) if rank == 0 else None
+    if world == 1:
+        MS.mssp_tile(dg, src[:64], out=tile[:64])  # warm
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        _, stats = MS.mssp_tile(dg, src, out=tile, stats=True)
+        e1.record()
+        torch.cuda.synchronize()
+        ms, transport = e0.elapsed_time(e1), "local"
+    else:
+        MS.apsp_sharded(dg, src[: 64 * world], "govm", tile=tile[: 64 * world] if tile is not None else None)  # warm
+        res = MS.apsp_sharded(dg, src, "govm", tile=tile)
+        ms, stats, transport = res.ms_max, res.stats, res.transport
+    if rank != 0:
+        return None
+    R = sum(s.relaxations for s in stats)
+    W = sum(s.writes for s in stats)
+    b_alg = 12 * R + 16 * (W + k) + 12 * W
+    peak, peak_src = hbm_peak()
+    t = ms / 1e3
+    # spot check: a few rows against single-source solves
+    import ctypes
+    from paper_2306_07872_b200 import _native as N
+
+    L = N.lib()
+    s = dg.solver(0)
+    d = torch.empty(dg.n, dtype=torch.float64, device=dev)
+    st = N.Stats()
+    for i in (0, k // 2, k - 1):
+        N.check(L.dawn_sssp(s, src[i], N.GOVM, 0, d.data_ptr(), None, ctypes.byref(st), torch.cuda.current_stream(
+            dev).cuda_stream))
+        if not torch.equal(d, tile[i].double()) or st.relaxations != stats[i].relaxations:
+            raise AssertionError(f"APSP row {i} disagrees with the single-source solve")
+    return {
+        "workload": f"C3: {k} sources on RMAT scale-{args.apsp_scale} ef16 float32 U[0,1) "
+                    f"({dg.n} nodes, {dg.m} edges)",
+        "metric": "APSP sources/s", "value": k / t, "unit": "sources/s", "n_gpus": world, "ms": ms,
+        "sources": k, "batch": MS.BATCH, "transport": transport,
+        "window": "first launch -> all float32 rows resident in rank 0's [k][n] tile (max over ranks)",
+        "relax_gps": R / t / 1e9, "relaxations": R,
+        "sssp_equiv_roofline": {"achieved": b_alg / t / 1e9, "peak": peak * world, "unit": "GB/s",
+                                "frac": b_alg / t / 1e9 / (peak * world), "peak_source": peak_src,
+                                "note": "sum over sources of the single-source algorithmic bytes (12R+16S+12W); "
+                                        "batching 32 sources amortises col/w reads, so this can exceed 1"},
+        "rows_checked": 3,
+    }
+
+
+# ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
 def ours(args):
@@ -326,24 +400,72 @@ def ours(args):
         except Exception:
             traffic = None
 
-    # end to end through the public API: resident graph (cached upload), source in,
-    # float64 distances + stats back to the host every step
+    # ---- end to end through the C ABI with HOST buffers (the reference-facing call) ----
+    # every step: the CsrGraph arrays in the reference's layout (int64 row_ptr,
+    # int64 col, float64 val; pinned host memory) go to the device
+    # (dawn_graph_create converts them in place over PCIe), the solve runs, the
+    # float64 distances come back to pinned host memory, and the graph is freed.
     e2e = None
+    e2e_resident = None
     if host is not None:
-        P.govm_sssp(host, src, precision="fp32")  # upload + warm
+        import ctypes as C
+
+        rp_h = torch.from_numpy(np.ascontiguousarray(host.row_ptr)).pin_memory()
+        col_h = torch.from_numpy(np.ascontiguousarray(host.col)).pin_memory()
+        val_h = torch.from_numpy(np.ascontiguousarray(host.val)).pin_memory()
+        out_h = torch.empty(n, dtype=torch.float64).pin_memory()
+        m_edges = int(host.m)
+        st_e = N.Stats()
+
+        def e2e_step():
+            h = C.c_void_p()
+            N.check(L.dawn_graph_create(local, n, m_edges, rp_h.data_ptr(), col_h.data_ptr(), val_h.data_ptr(),
+                                        N.F32, 0, C.byref(h)))
+            sv = C.c_void_p()
+            N.check(L.dawn_solver_create(h, 0, C.byref(sv)))
+            N.check(L.dawn_sssp(sv, src, N.GOVM, 0, out_h.data_ptr(), None, C.byref(st_e), stream))
+            N.check(L.dawn_solver_destroy(sv))
+            N.check(L.dawn_graph_destroy(h))
+
+        e2e_step()  # warm (context, module load)
         torch.cuda.synchronize()
-        KE = max(3, min(K, 20))
+        KE = max(3, min(K, 5))
+        if world > 1:
+            dist.barrier()
         t0 = time.perf_counter()
         for _ in range(KE):
-            dv, _, _st = P.govm_sssp(host, src, precision="fp32")
+            e2e_step()
+        torch.cuda.synchronize()
         t_e2e = (time.perf_counter() - t0) / KE
-        e2e = {"value": world * m_reach / t_e2e / 1e9, "unit": "GTEPS", "h2d_bytes_per_step": 0,
+        if world > 1:
+            tt = torch.tensor([t_e2e], device=dev, dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            t_e2e = float(tt.item())
+        h2d = 8 * (n + 1) + 16 * m_edges
+        e2e = {"value": world * m_reach / t_e2e / 1e9, "unit": "GTEPS", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": 8 * n + 48, "ms_per_step": 1e3 * t_e2e, "steps": KE,
-               "note": "P.govm_sssp(CsrGraph, 0, precision='fp32') with the graph resident (uploaded once, as the "
-                       "reference holds its CsrGraph in memory); the source is a kernel argument (0 bytes copied); "
-                       "D2H = float64 distances + counters"}
+               "note": "C ABI with host buffers per step: dawn_graph_create from pinned int64/int64/float64 CSR "
+                       "(reference CsrGraph layout, read in place over PCIe) + dawn_solver_create + dawn_sssp with "
+                       "float64 distances into pinned host memory + destroy; wall clock, max over ranks"}
+        if not np.array_equal(np.isfinite(out_h.numpy()), fin.cpu().numpy()):
+            raise AssertionError("C-ABI result disagrees with the timed device result")
+        # resident graph through the Python API (upload cached, as the reference holds its CsrGraph)
+        P.govm_sssp(host, src, precision="fp32")
+        torch.cuda.synchronize()
+        KR = max(3, min(K, 20))
+        t0 = time.perf_counter()
+        for _ in range(KR):
+            dv, _, _st = P.govm_sssp(host, src, precision="fp32")
+        t_res = (time.perf_counter() - t0) / KR
+        e2e_resident = {"value": world * m_reach / t_res / 1e9, "unit": "GTEPS", "ms_per_step": 1e3 * t_res,
+                        "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 8 * n + 48,
+                        "note": "P.govm_sssp(CsrGraph, 0, precision='fp32'), graph upload cached by identity"}
         if not np.array_equal(np.isfinite(dv.dist), fin.cpu().numpy()):
             raise AssertionError("public-API result disagrees with the timed device result")
+
+    apsp = None
+    if not args.no_apsp:
+        apsp = run_apsp(args, rank, world, local)
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline and host is not None:
@@ -371,6 +493,8 @@ def ours(args):
                                       "dist+frontier per write)"},
         "cpu_baseline": cpu,
         "e2e": e2e,
+        "e2e_resident": e2e_resident,
+        "apsp": apsp,
         "gpu_launches": 2 * K,
         "clocks": clocks,
         "relax_gps": world * R / t_step / 1e9,

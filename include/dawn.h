@@ -92,7 +92,9 @@ int dawn_choose_vtype(int64_t n, int64_t m, const double* val, int precision, in
 
 /* Upload an immutable CSR graph (CsrGraph, graph.py:64-109) to `device`.
  * row_ptr/col/val are host pointers unless src_is_device != 0, in which case
- * they are device pointers on `device`.  Weights are converted to `vtype`;
+ * they are device pointers on `device`.  Page-locked (pinned) host arrays are
+ * read in place by the conversion kernels over PCIe (no staging copy);
+ * pageable ones are staged through a temporary device buffer.  Weights are converted to `vtype`;
  * for integer vtypes a non-integral or out-of-range weight is DAWN_EINVAL
  * (never silently truncated, SURVEY §8(b) constraint 5). */
 int dawn_graph_create(int device, int64_t n, int64_t m, const int64_t* row_ptr,

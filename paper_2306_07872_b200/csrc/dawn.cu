@@ -137,6 +137,17 @@ static bool is_device_ptr(const void* p) {
   return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
+// page-locked host memory the device can read in place (UVA): the upload
+// kernels stream it over PCIe without a staging copy
+static bool is_pinned_host_ptr(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost && a.devicePointer != nullptr;
+}
+
 // ---------------------------------------------------------------------------
 // graph upload / conversion kernels
 // ---------------------------------------------------------------------------
@@ -314,7 +325,19 @@ extern "C" int dawn_graph_create(int device, int64_t n, int64_t m, const int64_t
   const double* d_val = val;
   void* tmp = nullptr;
   unsigned* d_flags = nullptr;
-  if (!src_is_device) {
+  const bool pinned = !src_is_device && is_pinned_host_ptr(row_ptr) && (m == 0 || (is_pinned_host_ptr(col) &&
+                                                                                   is_pinned_host_ptr(val)));
+  if (pinned) {
+    cudaPointerAttributes a;
+    cudaPointerGetAttributes(&a, row_ptr);
+    d_rp = (const int64_t*)a.devicePointer;
+    if (m) {
+      cudaPointerGetAttributes(&a, col);
+      d_col = (const int64_t*)a.devicePointer;
+      cudaPointerGetAttributes(&a, val);
+      d_val = (const double*)a.devicePointer;
+    }
+  } else if (!src_is_device) {
     const size_t bytes = 8 * (size_t)(n + 1) + 16 * (size_t)m;
     if ((e = cudaMalloc(&tmp, bytes)) != cudaSuccess)
       return cleanup(fail(DAWN_ENOMEM, "staging alloc: %s", cudaGetErrorString(e)));
