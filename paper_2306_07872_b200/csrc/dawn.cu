@@ -95,6 +95,7 @@ struct dawn_solver_s {
   int grid_pred = 1;  // ... of the predecessor-tracking instance
   size_t smem = 0;
   double dense_edges_per_node = 0.5;
+  uint32_t hot = 0;                   // tunable: nodes cached in shared memory in dense rounds
   double batch_min_sources = 4;       // tunable: dawn_mssp batches when k >= this  // tunable: dense frontier build after rounds relaxing >= this * n edges
   int ebits = 32;
   int logn = 0;
@@ -441,13 +442,12 @@ struct Impl {
     P.dense_edges = (unsigned long long)std::max(1.0, s->dense_edges_per_node * (double)g->n);
     P.prof = s->prof;
     P.prof_cap = s->prof_cap;
+    P.hot = s->hot;
     return P;
   }
 
-  static size_t smem_bytes() { return sizeof(Smem<V, EI>); }
-
   static int setup(dawn_solver_t s) {
-    const size_t sm = smem_bytes();
+    const size_t sm = sizeof(Smem<V, EI>) + sizeof(K) * (size_t)s->hot;
     const bool raw = !s->g->has_negative;
     auto k0 = raw ? dawn_persistent<V, EI, false, true> : dawn_persistent<V, EI, false, false>;
     auto k1 = raw ? dawn_persistent<V, EI, true, true> : dawn_persistent<V, EI, true, false>;
@@ -740,6 +740,15 @@ extern "C" int dawn_solver_tune(dawn_solver_t s, const char* key, double value) 
     if (!(value >= 0.0)) return fail(DAWN_EINVAL, "dense_edges_per_node must be >= 0");
     s->dense_edges_per_node = value;
     return DAWN_OK;
+  }
+  if (!strcmp(key, "hot_nodes")) {
+    if (!(value >= 0.0)) return fail(DAWN_EINVAL, "hot_nodes must be >= 0");
+    const uint32_t h = (uint32_t)std::min<double>(value, (double)s->g->n);
+    const size_t ks = (s->g->vtype == DAWN_I32 || s->g->vtype == DAWN_F32) ? 4 : 8;
+    if (ks * h > 160 * 1024) return fail(DAWN_EINVAL, "hot_nodes too large for shared memory");
+    s->hot = h;
+    CK(cudaSetDevice(s->g->device));
+    return DISPATCH(s->g, setup(s));
   }
   if (!strcmp(key, "batch_min_sources")) {
     if (!(value >= 0.0)) return fail(DAWN_EINVAL, "batch_min_sources must be >= 0");

@@ -14,7 +14,7 @@
 namespace dawn {
 
 #ifndef DAWN_MIN_BLOCKS
-#define DAWN_MIN_BLOCKS 3   // resident CTAs per SM the register budget is sized for
+#define DAWN_MIN_BLOCKS 2   // resident CTAs per SM the register budget is sized for (128 regs, no spills)
 #endif
 
 #ifndef DAWN_NT
