@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--out", default=None)
     ap.add_argument("--grid", type=int, default=0, help="grid side (>0: 2D grid instead of RMAT)")
     ap.add_argument("--dense", type=float, default=None, help="dense_edges_per_node tuning knob")
+    ap.add_argument("--bitmap", type=float, default=None, help="bitmap_edges_per_node tuning knob")
     a = ap.parse_args()
     import torch
 
@@ -45,6 +46,8 @@ def main():
     s = dg.solver(N.F_PROFILE)
     if a.dense is not None:
         N.check(L.dawn_solver_tune(s, b"dense_edges_per_node", a.dense))
+    if a.bitmap is not None:
+        N.check(L.dawn_solver_tune(s, b"bitmap_edges_per_node", a.bitmap))
     stream = torch.cuda.current_stream().cuda_stream
     algo = N.GOVM if a.algo == "govm" else N.GSVM
     times = []
