@@ -180,7 +180,9 @@ def apsp_sharded(g, sources: Sequence[int], algo: str = "govm", *, precision: st
         transport = "p2p" if on_gpu and backend == "nccl" else "collective"
     if transport == "p2p":
         # every rank must be able to reach the root's HBM; agree on it
-        ok = torch.tensor([1 if on_gpu and _p2p_possible(root if world > 1 else dev.index, dev.index) else 0],
+        rdev = [dev.index if on_gpu else -1]
+        dist.broadcast_object_list(rdev, src=root, group=group)
+        ok = torch.tensor([1 if on_gpu and rdev[0] >= 0 and _p2p_possible(rdev[0], dev.index) else 0],
                           device=dev if backend == "nccl" else "cpu")
         dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
         if int(ok.item()) == 0:
