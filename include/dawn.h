@@ -184,6 +184,16 @@ int dawn_batch_supported(dawn_solver_t s, int algo, unsigned flags, int* out);
 int dawn_mssp_batch(dawn_solver_t s, const int64_t* sources, int64_t k, int algo, unsigned flags,
                     void* dist_out, int out_vtype, int64_t ld, dawn_stats_t* stats_out, void* stream);
 
+/* Canonical CSR construction on the device — build_csr (reference
+ * graph.py:303-322): rows by source u, columns ascending, ties in input order,
+ * duplicates and self-loops kept, row_ptr[n+1].  Inputs u, v (int64), w
+ * (float64) of m edges are host (src_is_device = 0) or device arrays; outputs
+ * are host or device arrays of the reference CsrGraph layout (int64 row_ptr,
+ * int64 col, float64 val).  An endpoint outside [0, n) or a non-finite weight
+ * is DAWN_EINVAL (EdgeList.validate, graph.py:53-60).  Synchronises `stream`. */
+int dawn_build_csr(int device, int64_t n, int64_t m, const int64_t* u, const int64_t* v, const double* w,
+                   int src_is_device, int64_t* row_ptr_out, int64_t* col_out, double* val_out, void* stream);
+
 /* Synthetic generators on the device (SURVEY §8(f) row F1 inputs).  They
  * write an edge list (u, v, w) of m edges, deterministic in `seed` through a
  * counter-based hash, identical to the host restatement in

@@ -56,6 +56,7 @@ EXPORTS = (
     "dawn_mssp",
     "dawn_batch_supported",
     "dawn_mssp_batch",
+    "dawn_build_csr",
     "dawn_gen_rmat",
 )
 
@@ -103,6 +104,8 @@ def _declare(L: ctypes.CDLL) -> None:
         "dawn_batch_supported": (c_int, [c_void_p, c_int, c_uint, POINTER(c_int)]),
         "dawn_mssp_batch": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_uint, c_void_p, c_int, c_int64,
                                     c_void_p, c_void_p]),
+        "dawn_build_csr": (c_int, [c_int, c_int64, c_int64, c_void_p, c_void_p, c_void_p, c_int, c_void_p, c_void_p,
+                                   c_void_p, c_void_p]),
         "dawn_gen_rmat": (c_int, [c_int, c_int, c_int64, c_double, c_double, c_double, c_uint64, c_int,
                                   c_int64, c_int64, c_uint64, c_void_p, c_void_p, c_void_p, c_void_p]),
     }

@@ -22,6 +22,7 @@
 
 #include "../../include/dawn.h"
 #include "dawn_batch.cuh"
+#include "dawn_csr.cuh"
 
 using namespace dawn;
 
@@ -989,6 +990,108 @@ extern "C" int dawn_mssp(dawn_solver_t s, const int64_t* sources, int64_t k, int
     for (int64_t i = 0; i < k; ++i) fill_stats(hs[i], stats_out + i);
   if (hs) cudaFreeHost(hs);
   return rc;
+}
+
+// ---------------------------------------------------------------------------
+// canonical CSR construction (build_csr, graph.py:303-322) on the device
+// ---------------------------------------------------------------------------
+static int bits_for(unsigned long long x) {
+  int b = 0;
+  while (b < 64 && (x >> b) != 0ull) ++b;
+  return b;
+}
+
+extern "C" int dawn_build_csr(int device, int64_t n, int64_t m, const int64_t* u, const int64_t* v,
+                              const double* w, int src_is_device, int64_t* row_ptr_out, int64_t* col_out,
+                              double* val_out, void* stream) {
+  if (n < 0 || m < 0 || !row_ptr_out || (m > 0 && (!u || !v || !w || !col_out || !val_out)))
+    return fail(DAWN_EINVAL, "bad build_csr arguments (n=%lld, m=%lld)", (long long)n, (long long)m);
+  if (n > 0 && (unsigned long long)n > 0xFFFFFFFFull)
+    return fail(DAWN_EUNSUPPORTED, "n=%lld exceeds the 2^32 node limit of the 64-bit sort key", (long long)n);
+  CK(cudaSetDevice(device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const bool out_dev = is_device_ptr(row_ptr_out);
+  const int blocks = 148 * 8;
+  if (m == 0) {
+    if (out_dev) {
+      k_csr_empty<<<blocks, 256, 0, st>>>(n, row_ptr_out);
+      CK(cudaGetLastError());
+      CK(cudaStreamSynchronize(st));
+    } else {
+      memset(row_ptr_out, 0, 8 * (size_t)(n + 1));
+    }
+    return DAWN_OK;
+  }
+  // device workspace: staged inputs (host sources), keys/idx in and out, outputs, temp storage
+  size_t tmp_bytes = 0;
+  CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, (const unsigned long long*)nullptr,
+                                     (unsigned long long*)nullptr, (const unsigned long long*)nullptr,
+                                     (unsigned long long*)nullptr, m, 0, 64, st));
+  const size_t in_bytes = src_is_device ? 0 : 24 * (size_t)m;
+  const size_t out_bytes = out_dev ? 0 : 8 * (size_t)(n + 1) + 16 * (size_t)m;
+  const size_t total = in_bytes + 32 * (size_t)m + out_bytes + tmp_bytes + 64;
+  char* ws = nullptr;
+  CK(cudaMalloc(&ws, total));
+  auto release = [&](int rc) { cudaFree(ws); return rc; };
+  char* q = ws;
+  const int64_t* du = u;
+  const int64_t* dv = v;
+  const double* dw = w;
+  cudaError_t e;
+  if (!src_is_device) {
+    int64_t* su = (int64_t*)q;
+    int64_t* sv = su + m;
+    double* sw = (double*)(sv + m);
+    q += in_bytes;
+    if ((e = cudaMemcpyAsync(su, u, 8 * (size_t)m, cudaMemcpyDefault, st)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(sv, v, 8 * (size_t)m, cudaMemcpyDefault, st)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(sw, w, 8 * (size_t)m, cudaMemcpyDefault, st)) != cudaSuccess)
+      return release(fail(DAWN_ECUDA, "edge upload: %s", cudaGetErrorString(e)));
+    du = su;
+    dv = sv;
+    dw = sw;
+  }
+  unsigned long long* k0 = (unsigned long long*)q;
+  unsigned long long* k1 = k0 + m;
+  unsigned long long* i0 = k1 + m;
+  unsigned long long* i1 = i0 + m;
+  q += 32 * (size_t)m;
+  int64_t* rp = row_ptr_out;
+  int64_t* col = col_out;
+  double* val = val_out;
+  if (!out_dev) {
+    rp = (int64_t*)q;
+    col = rp + (n + 1);
+    val = (double*)(col + m);
+    q += out_bytes;
+  }
+  void* tmp = q;
+  q += tmp_bytes;
+  unsigned* flags = (unsigned*)(((uintptr_t)q + 15) & ~(uintptr_t)15);
+  if ((e = cudaMemsetAsync(flags, 0, sizeof(unsigned), st)) != cudaSuccess)
+    return release(fail(DAWN_ECUDA, "flags: %s", cudaGetErrorString(e)));
+  k_csr_keys<<<blocks, 256, 0, st>>>(du, dv, dw, n, m, k0, i0, flags);
+  if ((e = cudaGetLastError()) != cudaSuccess) return release(fail(DAWN_ECUDA, "keys: %s", cudaGetErrorString(e)));
+  const int kbits = std::max(1, bits_for((unsigned long long)n * (unsigned long long)n - 1ull));
+  if ((e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, k0, k1, i0, i1, m, 0, kbits, st)) != cudaSuccess)
+    return release(fail(DAWN_ECUDA, "sort: %s", cudaGetErrorString(e)));
+  k_csr_emit<<<blocks, 256, 0, st>>>(k1, i1, dw, n, m, col, val);
+  k_csr_rowptr<<<blocks, 256, 0, st>>>(k1, n, m, rp);
+  if ((e = cudaGetLastError()) != cudaSuccess) return release(fail(DAWN_ECUDA, "emit: %s", cudaGetErrorString(e)));
+  unsigned hflags = 0;
+  if ((e = cudaMemcpyAsync(&hflags, flags, sizeof(unsigned), cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
+      (e = cudaStreamSynchronize(st)) != cudaSuccess)
+    return release(fail(DAWN_ECUDA, "build_csr: %s", cudaGetErrorString(e)));
+  if (hflags & CSR_ERR_NODE) return release(fail(DAWN_EINVAL, "edge endpoint out of range for n=%lld", (long long)n));
+  if (hflags & CSR_ERR_WEIGHT) return release(fail(DAWN_EINVAL, "non-finite edge weight"));
+  if (!out_dev) {
+    if ((e = cudaMemcpyAsync(row_ptr_out, rp, 8 * (size_t)(n + 1), cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(col_out, col, 8 * (size_t)m, cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(val_out, val, 8 * (size_t)m, cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
+        (e = cudaStreamSynchronize(st)) != cudaSuccess)
+      return release(fail(DAWN_ECUDA, "csr download: %s", cudaGetErrorString(e)));
+  }
+  return release(DAWN_OK);
 }
 
 // ---------------------------------------------------------------------------

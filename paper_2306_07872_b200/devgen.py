@@ -1,12 +1,12 @@
-"""Device-side synthetic graph construction for large configurations.
+"""Device-side graph construction.
 
 ``dawn_gen_rmat`` (csrc/dawn.cu) draws the RMAT edge list on the GPU with the
 same counter hash as :mod:`generators` (so the graph is bit-identical to the
-host restatement), then the canonical CSR order — rows by source, columns
-ascending, ties in generation order (reference graph.py:303-322) — comes from
-a stable device sort of the 64-bit key ``u*n + v``.  torch supplies the sort
-and buffers here (plumbing); the graph is handed to ``dawn_graph_create``
-without a host round trip.
+host restatement); ``dawn_build_csr`` (csrc/dawn_csr.cuh) then puts any edge
+list in the canonical CSR order of the reference's ``build_csr`` — rows by
+source, columns ascending, ties in input order (graph.py:303-322) — with a
+stable device radix sort of the 64-bit key ``u*n + v``.  torch only holds
+the buffers; the graph reaches ``dawn_graph_create`` without a host round trip.
 """
 
 from __future__ import annotations
@@ -14,6 +14,44 @@ from __future__ import annotations
 from . import _native as N
 from .device import DeviceGraph
 from .graph import CsrGraph
+
+
+def csr_device(n: int, u, v, w, device: int = 0):
+    """Canonical CSR (reference build_csr order, graph.py:303-322) built on the
+    device by ``dawn_build_csr``: int64 ``row_ptr[n+1]``, int64 ``col[m]``,
+    float64 ``val[m]`` CUDA tensors.  ``u``/``v``/``w`` are CUDA tensors or
+    host arrays (int64, int64, float64)."""
+    import numpy as np
+    import torch
+
+    dev = torch.device("cuda", device)
+    on_dev = isinstance(u, torch.Tensor) and u.is_cuda
+    if on_dev:
+        u = u.to(torch.int64).contiguous()
+        v = v.to(torch.int64).contiguous()
+        w = w.to(torch.float64).contiguous()
+        m = int(u.numel())
+        pu, pv, pw = u.data_ptr(), v.data_ptr(), w.data_ptr()
+    else:
+        u = np.ascontiguousarray(u, dtype=np.int64)
+        v = np.ascontiguousarray(v, dtype=np.int64)
+        w = np.ascontiguousarray(w, dtype=np.float64)
+        m = int(u.size)
+        pu, pv, pw = (u.ctypes.data, v.ctypes.data, w.ctypes.data) if m else (None, None, None)
+    row_ptr = torch.empty(n + 1, dtype=torch.int64, device=dev)
+    col = torch.empty(max(m, 1), dtype=torch.int64, device=dev)
+    val = torch.empty(max(m, 1), dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    N.check(N.lib().dawn_build_csr(device, n, m, pu, pv, pw, 1 if on_dev else 0, row_ptr.data_ptr(),
+                                   col.data_ptr(), val.data_ptr(), stream))
+    return row_ptr, col[:m], val[:m]
+
+
+def build_csr_device(n: int, u, v, w, device: int = 0) -> CsrGraph:
+    """``build_csr`` on the GPU, returned as the reference's host ``CsrGraph``."""
+    rp, col, val = csr_device(n, u, v, w, device=device)
+    return CsrGraph(n=n, m=int(col.numel()), row_ptr=rp.cpu().numpy(), col=col.cpu().numpy(),
+                    val=val.cpu().numpy())
 
 
 def rmat_csr_device(scale: int, edge_factor: int, weights: str = "f32", lo: int = 1, hi: int = 100, seed: int = 1,
@@ -30,15 +68,8 @@ def rmat_csr_device(scale: int, edge_factor: int, weights: str = "f32", lo: int 
     stream = torch.cuda.current_stream(dev).cuda_stream
     N.check(N.lib().dawn_gen_rmat(device, scale, edge_factor, a, b, c, seed, 0 if weights == "int" else 1, lo, hi,
                                   wseed, u.data_ptr(), v.data_ptr(), w.data_ptr(), stream))
-    key = u * n + v
-    _, order = torch.sort(key, stable=True)
-    del key
-    col = v[order]
-    val = w[order]
-    counts = torch.bincount(u, minlength=n)
-    del u, v, w, order
-    row_ptr = torch.zeros(n + 1, dtype=torch.int64, device=dev)
-    torch.cumsum(counts, 0, out=row_ptr[1:])
+    row_ptr, col, val = csr_device(n, u, v, w, device=device)
+    del u, v, w
     return n, m, row_ptr, col, val
 
 
