@@ -113,7 +113,10 @@ int dawn_solver_destroy(dawn_solver_t s);
  *   "dense_edges_per_node" (default 0.5): a round that relaxes at least
  *   value*n edges records its writes as plain stamps and the next frontier is
  *   rebuilt by a coalesced sweep; lighter rounds enqueue written nodes.
- *   "batch_min_sources" (default 4): dawn_mssp batches k >= value sources. */
+ *   "batch_min_sources" (default 4): dawn_mssp batches k >= value sources.
+ *   "wide_tiles" (default -1 = auto): 1 / 0 forces wide (14 edges per lane)
+ *   or narrow (8) X-phase warp tiles for 4-byte values; auto = wide when
+ *   m >= 2^25 and m >= 8n. */
 int dawn_solver_tune(dawn_solver_t s, const char* key, double value);
 
 /* One single-source solve: govm_sssp / gsvm_sssp (solver.py:265-399),

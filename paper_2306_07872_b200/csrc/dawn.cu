@@ -96,7 +96,8 @@ struct dawn_solver_s {
   int grid_pred = 1;  // ... of the predecessor-tracking instance
   size_t smem = 0;
   double dense_edges_per_node = 0.5;
-  uint32_t hot = 0;                   // tunable: nodes cached in shared memory in dense rounds
+  int wide_pref = -1;                 // tunable "wide_tiles": -1 auto, 0 narrow, 1 wide X-phase tiles
+  bool wide = false;
   double batch_min_sources = 4;       // tunable: dawn_mssp batches when k >= this  // tunable: dense frontier build after rounds relaxing >= this * n edges
   int ebits = 32;
   int logn = 0;
@@ -443,15 +444,29 @@ struct Impl {
     P.dense_edges = (unsigned long long)std::max(1.0, s->dense_edges_per_node * (double)g->n);
     P.prof = s->prof;
     P.prof_cap = s->prof_cap;
-    P.hot = s->hot;
     return P;
   }
 
-  static int setup(dawn_solver_t s) {
-    const size_t sm = sizeof(Smem<V, EI>) + sizeof(K) * (size_t)s->hot;
+  // tile width of the X phase: wide (XI_WIDE edges per lane) for 4-byte values
+  // on graphs with heavy rounds, narrow (8) otherwise
+  static constexpr int XW = sizeof(K) == 4 ? XI_WIDE : XI_NARROW;
+  template <int XI>
+  static void* kernel(bool pred, bool raw) {
+    if (pred) return raw ? (void*)dawn_persistent<V, EI, true, true, XI> : (void*)dawn_persistent<V, EI, true, false, XI>;
+    return raw ? (void*)dawn_persistent<V, EI, false, true, XI> : (void*)dawn_persistent<V, EI, false, false, XI>;
+  }
+  static void* kernel_for(dawn_solver_t s, bool pred) {
     const bool raw = !s->g->has_negative;
-    auto k0 = raw ? dawn_persistent<V, EI, false, true> : dawn_persistent<V, EI, false, false>;
-    auto k1 = raw ? dawn_persistent<V, EI, true, true> : dawn_persistent<V, EI, true, false>;
+    return s->wide ? kernel<XW>(pred, raw) : kernel<XI_NARROW>(pred, raw);
+  }
+
+  static int setup(dawn_solver_t s) {
+    const int64_t n = s->g->n, m = s->g->m;
+    if (s->wide_pref < 0) s->wide = XW != XI_NARROW && m >= (1ll << 25) && m >= 8 * n;
+    else s->wide = XW != XI_NARROW && s->wide_pref > 0;
+    const size_t sm = s->wide ? sizeof(Smem<V, EI, XW>) : sizeof(Smem<V, EI, XI_NARROW>);
+    const void* k0 = kernel_for(s, false);
+    const void* k1 = kernel_for(s, true);
     CK(cudaFuncSetAttribute(k0, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     CK(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     // Keep the shared-memory carveout to what DAWN_MIN_BLOCKS resident CTAs
@@ -469,7 +484,6 @@ struct Impl {
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps0, k0, NT, sm));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps1, k1, NT, sm));
     if (bps0 < 1 || bps1 < 1) return fail(DAWN_ECUDA, "persistent kernel cannot be resident (smem %zu)", sm);
-    const int64_t n = s->g->n, m = s->g->m;
     const int64_t work = std::max<int64_t>((n + TILE - 1) / TILE, (m + TILE - 1) / TILE);
     s->grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)bps0 * nsm, work));
     s->grid_pred = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)bps1 * nsm, work));
@@ -494,10 +508,7 @@ struct Impl {
   static int run(dawn_solver_t s, unsigned max_rounds, cudaStream_t stream) {
     KParams<V, EI> P = params(s, max_rounds);
     void* args[] = {&P};
-    const bool raw = !s->g->has_negative;
-    void* fn;
-    if (P.pred_on) fn = raw ? (void*)dawn_persistent<V, EI, true, true> : (void*)dawn_persistent<V, EI, true, false>;
-    else fn = raw ? (void*)dawn_persistent<V, EI, false, true> : (void*)dawn_persistent<V, EI, false, false>;
+    void* fn = kernel_for(s, P.pred_on != 0);
     CK(cudaLaunchCooperativeKernel(fn, dim3(P.pred_on ? s->grid_pred : s->grid), dim3(NT), args, s->smem,
                                    stream));
     return DAWN_OK;
@@ -653,7 +664,7 @@ struct Impl {
       CK(cudaMalloc(&s->qbase[i], es * n));
       CK(cudaMalloc(&s->qkey[i], ks * n));
     }
-    CK(cudaMalloc(&s->tile_row, 4 * (size_t)(m / WT + 4)));
+    CK(cudaMalloc(&s->tile_row, 4 * (size_t)(m / WT_MIN + 4)));
     CK(cudaMalloc(&s->st, sizeof(DevState)));
     CK(cudaMemset(s->st, 0, sizeof(DevState)));
     CK(cudaMallocHost(&s->st_host, sizeof(DevState)));
@@ -742,12 +753,9 @@ extern "C" int dawn_solver_tune(dawn_solver_t s, const char* key, double value) 
     s->dense_edges_per_node = value;
     return DAWN_OK;
   }
-  if (!strcmp(key, "hot_nodes")) {
-    if (!(value >= 0.0)) return fail(DAWN_EINVAL, "hot_nodes must be >= 0");
-    const uint32_t h = (uint32_t)std::min<double>(value, (double)s->g->n);
-    const size_t ks = (s->g->vtype == DAWN_I32 || s->g->vtype == DAWN_F32) ? 4 : 8;
-    if (ks * h > 160 * 1024) return fail(DAWN_EINVAL, "hot_nodes too large for shared memory");
-    s->hot = h;
+  if (!strcmp(key, "wide_tiles")) {
+    if (!(value == -1.0 || value == 0.0 || value == 1.0)) return fail(DAWN_EINVAL, "wide_tiles must be -1, 0 or 1");
+    s->wide_pref = (int)value;
     CK(cudaSetDevice(s->g->device));
     return DISPATCH(s->g, setup(s));
   }

@@ -64,23 +64,33 @@ struct KParams {
   unsigned long long dense_edges;      // a round relaxing >= this many edges builds the next frontier densely
   unsigned long long* prof;            // optional per-round timeline (4 words/round) or nullptr
   unsigned prof_cap;                   // rounds the timeline can hold
-  uint32_t hot;                        // nodes [0, hot) cached in shared memory during dense rounds (0 = off)
 };
 
 constexpr int WPB = NT / 32;       // warps per CTA
-constexpr int WT = 32 * ITEMS;     // virtual edges per warp tile (256)
+// Virtual edges per lane of a warp tile in the X phase (template XI): as many
+// independent edge loads + dist gathers in flight per lane as the 128-register
+// budget holds without spilling.  Two widths are instantiated for 4-byte
+// values: XI_WIDE (14, best of 8/10/12/14/16 on C2) for graphs with heavy
+// rounds, 8 otherwise (the grid and small graphs prefer more, smaller tiles;
+// profiles/r01_experiments.md).  8-byte values always use 8.
+#ifndef DAWN_XITEMS_WIDE
+#define DAWN_XITEMS_WIDE 14
+#endif
+constexpr int XI_NARROW = 8;
+constexpr int XI_WIDE = DAWN_XITEMS_WIDE;
+constexpr int WT_MIN = 32 * (XI_NARROW < XI_WIDE ? XI_NARROW : XI_WIDE);
 
 // Per-warp shared memory is only the row-start marks of a short-row tile
 // (512 B): everything else stays in registers or is read through L1, so the
 // shared-memory carveout stays minimal and L1 keeps ~200 KB for dist[] gathers.
-template <class V, class EI>
+template <int XI>
 struct __align__(16) WarpRows {
-  uint16_t mark[WT];            // row-start marks -> per-edge row index (max-scan)
+  uint16_t mark[32 * XI];       // row-start marks -> per-edge row index (max-scan)
 };
 
-template <class V, class EI>
+template <class V, class EI, int XI>
 struct __align__(16) Smem {
-  WarpRows<V, EI> w[WPB];
+  WarpRows<XI> w[WPB];
   unsigned long long scr64[WPB];
   unsigned long long basepk;
 };
@@ -119,8 +129,9 @@ __device__ __forceinline__ unsigned long long pk_edges(unsigned long long pk, in
 }
 
 // mark the warp tiles whose first virtual edge falls inside [off, off + deg)
-template <class EI>
+template <int XI, class EI>
 __device__ __forceinline__ void mark_tiles(uint32_t* tile_row, EI off, EI deg, uint32_t entry) {
+  constexpr int WT = 32 * XI;
   EI t0 = (off + (EI)(WT - 1)) / (EI)WT;
   EI t1 = (off + deg - 1) / (EI)WT;
   for (EI t = t0; t <= t1; ++t) tile_row[t] = entry;
@@ -139,7 +150,7 @@ __device__ __forceinline__ void count_write(uint8_t* wstate, uint32_t v, unsigne
 // ---------------------------------------------------------------------------
 // S phase, sparse: snapshot the queue the previous X phase built
 // ---------------------------------------------------------------------------
-template <class V, class EI>
+template <class V, class EI, int XI>
 __device__ void phase_snapshot(const KParams<V, EI>& P, int p) {
   const unsigned long long pk = ldcg(&P.st->res[p]);
   const uint32_t cnt = (uint32_t)pk_count(pk, P.ebits);
@@ -151,7 +162,7 @@ __device__ void phase_snapshot(const KParams<V, EI>& P, int p) {
     P.qkey[p][i] = ldcg(P.dist + u);
     const EI off = ldcg(qo + i);
     const EI nxt = (i + 1 < cnt) ? ldcg(qo + i + 1) : E;
-    mark_tiles<EI>(P.tile_row, off, nxt - off, i);
+    mark_tiles<XI, EI>(P.tile_row, off, nxt - off, i);
   }
 }
 
@@ -194,8 +205,8 @@ __device__ __forceinline__ void ldg8(const T* p, T (&o)[ITEMS]) {
   }
 }
 
-template <class V, class EI>
-__device__ void phase_compact(const KParams<V, EI>& P, int p, uint32_t r, Smem<V, EI>& s,
+template <class V, class EI, int XI>
+__device__ void phase_compact(const KParams<V, EI>& P, int p, uint32_t r, Smem<V, EI, XI>& s,
                               unsigned long long& acc_w, unsigned long long& acc_fd,
                               unsigned long long& acc_multi, uint32_t& prev_w) {
   using VT = Val<V>;
@@ -301,7 +312,7 @@ __device__ void phase_compact(const KParams<V, EI>& P, int p, uint32_t r, Smem<V
           P.qoff[p][pos] = off;
           P.qbase[p][pos] = rp[j] - off;
           P.qkey[p][pos] = keys[j];
-          mark_tiles<EI>(P.tile_row, off, deg, pos);
+          mark_tiles<XI, EI>(P.tile_row, off, deg, pos);
           pos++;
           off += deg;
         }
@@ -328,14 +339,15 @@ __device__ void phase_compact(const KParams<V, EI>& P, int p, uint32_t r, Smem<V
 // ---------------------------------------------------------------------------
 constexpr uint32_t SENT = 0xFFFFFFFFu;
 
-template <class V, class EI, bool PRED, bool RAW>
-__device__ void phase_expand(const KParams<V, EI>& P, int p, uint32_t r, bool dense, Smem<V, EI>& s,
+template <class V, class EI, bool PRED, bool RAW, int XI>
+__device__ void phase_expand(const KParams<V, EI>& P, int p, uint32_t r, bool dense, Smem<V, EI, XI>& s,
                              unsigned long long& acc_w, unsigned long long& acc_fd,
                              unsigned long long& acc_multi, uint32_t& round_w) {
   using CD = Codec<V, RAW>;
   using K = typename CD::K;
   using WB = typename CD::WB;
   using C = typename CD::C;
+  constexpr int WT = 32 * XI;
   const unsigned long long pk = ldcg(&P.st->res[p]);
   const uint32_t cnt = (uint32_t)pk_count(pk, P.ebits);
   const EI E = (EI)pk_edges(pk, P.ebits);
@@ -345,7 +357,7 @@ __device__ void phase_expand(const KParams<V, EI>& P, int p, uint32_t r, bool de
   const EI GW = (EI)gridDim.x * WPB;
   EI t = (EI)blockIdx.x * WPB + wid;
   if (t >= T) return;  // warp-uniform; no CTA barrier below
-  WarpRows<V, EI>& w = s.w[wid];
+  WarpRows<XI>& w = s.w[wid];
   const int np = p ^ 1;
   const int eb = P.ebits;
   const uint32_t src = P.src;
@@ -385,7 +397,8 @@ __device__ void phase_expand(const KParams<V, EI>& P, int p, uint32_t r, bool de
     const uint32_t c_rst = (lane < nrows) ? (uint32_t)(pf_off > e0 ? pf_off - e0 : (EI)0) : 0xFFFFFFFFu;
     if (!fast) {
       // ---- short rows: mark row starts (row data is read through L1 below) ----
-      reinterpret_cast<uint4*>(w.mark)[lane] = make_uint4(0, 0, 0, 0);
+#pragma unroll
+      for (int q = 0; q < XI; ++q) w.mark[lane * XI + q] = 0;
       __syncwarp();
       if (c_rst < len) w.mark[c_rst] = (uint16_t)lane;
       for (uint32_t k = 32 + lane; k < nrows; k += 32) {
@@ -412,13 +425,13 @@ __device__ void phase_expand(const KParams<V, EI>& P, int p, uint32_t r, bool de
     }
     if (!fast) {
       __syncwarp();
-      // inclusive max-scan of the marks: each lane owns ITEMS consecutive slots
-      const uint4 mv = reinterpret_cast<uint4*>(w.mark)[lane];
-      uint32_t m8[8] = {mv.x & 0xFFFFu, mv.x >> 16, mv.y & 0xFFFFu, mv.y >> 16,
-                        mv.z & 0xFFFFu, mv.z >> 16, mv.w & 0xFFFFu, mv.w >> 16};
+      // inclusive max-scan of the marks: each lane owns XI consecutive slots
+      uint32_t m8[XI];
+#pragma unroll
+      for (int j = 0; j < XI; ++j) m8[j] = w.mark[lane * XI + j];
       uint32_t run = 0;
 #pragma unroll
-      for (int j = 0; j < 8; ++j) { run = max(run, m8[j]); m8[j] = run; }
+      for (int j = 0; j < XI; ++j) { run = max(run, m8[j]); m8[j] = run; }
       uint32_t incl = run;
 #pragma unroll
       for (int d = 1; d < 32; d <<= 1) {
@@ -428,21 +441,18 @@ __device__ void phase_expand(const KParams<V, EI>& P, int p, uint32_t r, bool de
       uint32_t pre = __shfl_up_sync(0xffffffffu, incl, 1);
       if (lane == 0) pre = 0;
 #pragma unroll
-      for (int j = 0; j < 8; ++j) m8[j] = max(m8[j], pre);
-      reinterpret_cast<uint4*>(w.mark)[lane] =
-          make_uint4(m8[0] | (m8[1] << 16), m8[2] | (m8[3] << 16), m8[4] | (m8[5] << 16),
-                     m8[6] | (m8[7] << 16));
+      for (int j = 0; j < XI; ++j) w.mark[lane * XI + j] = (uint16_t)max(m8[j], pre);
       __syncwarp();
     }
 
     // ---- phase 1a: row of every edge (collectives / L1 only, no edge loads yet) ----
-    EI pos[ITEMS];
-    C rv[ITEMS];          // row value (decoded once per row)
-    uint32_t rowk[ITEMS];
+    EI pos[XI];
+    C rv[XI];          // row value (decoded once per row)
+    uint32_t rowk[XI];
     if (fast) {
       uint32_t before = 0;  // rows starting before the current 32-edge window
 #pragma unroll
-      for (int j = 0; j < ITEMS; ++j) {
+      for (int j = 0; j < XI; ++j) {
         const uint32_t lo = j * 32;
         const uint32_t bit = (c_rst - lo < 32u) ? (1u << (c_rst - lo)) : 0u;
         const uint32_t B = __reduce_or_sync(0xffffffffu, bit);
@@ -454,7 +464,7 @@ __device__ void phase_expand(const KParams<V, EI>& P, int p, uint32_t r, bool de
       }
     } else {
 #pragma unroll
-      for (int j = 0; j < ITEMS; ++j) {
+      for (int j = 0; j < XI; ++j) {
         // queue entries were written before the last grid barrier, whose fence
         // invalidated L1: L1-cached reads are coherent here
         const uint32_t k = w.mark[j * 32 + lane];
@@ -464,23 +474,23 @@ __device__ void phase_expand(const KParams<V, EI>& P, int p, uint32_t r, bool de
       }
     }
     // ---- phase 1b: all edge loads back to back (nothing consumes them yet) ----
-    uint32_t col[ITEMS];
-    WB wv[ITEMS];
-    unsigned okm = 0xFFu;  // items inside the tile
+    uint32_t col[XI];
+    WB wv[XI];
+    unsigned okm = (XI >= 32) ? 0xFFFFFFFFu : ((1u << XI) - 1u);  // items inside the tile
     if (len != (uint32_t)WT) {
       okm = 0;
 #pragma unroll
-      for (int j = 0; j < ITEMS; ++j) okm |= (unsigned)(j * 32 + lane < len) << j;
+      for (int j = 0; j < XI; ++j) okm |= (unsigned)(j * 32 + lane < len) << j;
     }
     {
       const EI safe0 = __shfl_sync(0xffffffffu, c_base, 0) + e0;  // the tile's first edge
 #pragma unroll
-      for (int j = 0; j < ITEMS; ++j) EdgeAccess<V>::load(P, ((okm >> j) & 1u) ? pos[j] : safe0, col[j], wv[j]);
+      for (int j = 0; j < XI; ++j) EdgeAccess<V>::load(P, ((okm >> j) & 1u) ? pos[j] : safe0, col[j], wv[j]);
     }
     // ---- phase 2: candidates ----
-    K cand[ITEMS];
+    K cand[XI];
 #pragma unroll
-    for (int j = 0; j < ITEMS; ++j) {
+    for (int j = 0; j < XI; ++j) {
       cand[j] = CD::relax(rv[j], wv[j]);
       if (!CD::usable(cand[j])) okm &= ~(1u << j);
     }
@@ -493,12 +503,12 @@ __device__ void phase_expand(const KParams<V, EI>& P, int p, uint32_t r, bool de
       // (CCTL.IVALL) and no gather is outstanding at a barrier, so a value
       // seen in L1 during round r was read after round r began and is <= the
       // round-start value.
-      K cur[ITEMS];
+      K cur[XI];
 #pragma unroll
-      for (int j = 0; j < ITEMS; ++j) cur[j] = ((okm >> j) & 1u) ? __ldca(P.dist + col[j]) : (K)0;
+      for (int j = 0; j < XI; ++j) cur[j] = ((okm >> j) & 1u) ? __ldca(P.dist + col[j]) : (K)0;
       unsigned need = 0;
 #pragma unroll
-      for (int j = 0; j < ITEMS; ++j) {
+      for (int j = 0; j < XI; ++j) {
         if (((okm >> j) & 1u) && cand[j] < cur[j]) {
           if (col[j] == src) P.st->flag = 1u;  // source guard (solver.py:299-303, :374-376, :236-239)
           else need |= 1u << j;
@@ -507,25 +517,25 @@ __device__ void phase_expand(const KParams<V, EI>& P, int p, uint32_t r, bool de
       // ---- phase 4: fire-and-forget min (cand < cur proves v is lowered this round) ----
       if (need) {
 #pragma unroll
-        for (int j = 0; j < ITEMS; ++j)
+        for (int j = 0; j < XI; ++j)
           if ((need >> j) & 1u) atomicMin(P.dist + col[j], cand[j]);
       }
       if (dense) {
         if (need) {
 #pragma unroll
-          for (int j = 0; j < ITEMS; ++j)
+          for (int j = 0; j < XI; ++j)
             if ((need >> j) & 1u) P.stamp[col[j]] = r;
         }
       } else if (__any_sync(0xffffffffu, need != 0u)) {
         // ---- sparse: elect one writer per (node, round), enqueue its row ----
         unsigned first = 0;
 #pragma unroll
-        for (int j = 0; j < ITEMS; ++j)
+        for (int j = 0; j < XI; ++j)
           if (((need >> j) & 1u) && atomicExch(P.stamp + col[j], r) != r) first |= 1u << j;
         unsigned long long mine = 0;  // (entries << eb) | edges of this lane
-        EI rs[ITEMS];
+        EI rs[XI];
 #pragma unroll
-        for (int j = 0; j < ITEMS; ++j) {
+        for (int j = 0; j < XI; ++j) {
           rs[j] = 0;
           if ((first >> j) & 1u) {
             round_w++;
@@ -556,7 +566,7 @@ __device__ void phase_expand(const KParams<V, EI>& P, int p, uint32_t r, bool de
           uint32_t pos = (uint32_t)pk_count(at, eb);
           EI off = (EI)pk_edges(at, eb);
 #pragma unroll
-          for (int j = 0; j < ITEMS; ++j) {
+          for (int j = 0; j < XI; ++j) {
             if ((first >> j) & 1u) {
               P.qnode[np][pos] = col[j];
               P.qoff[np][pos] = off;
@@ -568,15 +578,15 @@ __device__ void phase_expand(const KParams<V, EI>& P, int p, uint32_t r, bool de
         }
       }
     } else {
-      unsigned sv[ITEMS];
+      unsigned sv[XI];
 #pragma unroll
-      for (int j = 0; j < ITEMS; ++j)
+      for (int j = 0; j < XI; ++j)
         sv[j] = (((okm >> j) & 1u) && col[j] != src) ? ldcg(P.stamp + col[j]) : 0u;
-      K dv[ITEMS];
+      K dv[XI];
 #pragma unroll
-      for (int j = 0; j < ITEMS; ++j) dv[j] = (sv[j] == r) ? ldcg(P.dist + col[j]) : (K)0;
+      for (int j = 0; j < XI; ++j) dv[j] = (sv[j] == r) ? ldcg(P.dist + col[j]) : (K)0;
 #pragma unroll
-      for (int j = 0; j < ITEMS; ++j) {
+      for (int j = 0; j < XI; ++j) {
         const uint32_t u = fast ? __shfl_sync(0xffffffffu, c_node, rowk[j]) : __ldca(qnode + ci0 + rowk[j]);
         if (sv[j] == r && ((okm >> j) & 1u) && col[j] != src && cand[j] == dv[j])
           atomicMax(P.pred + col[j], ((unsigned long long)r << 32) | (unsigned long long)(~u));
@@ -586,274 +596,6 @@ __device__ void phase_expand(const KParams<V, EI>& P, int p, uint32_t r, bool de
   }
 }
 
-// ---------------------------------------------------------------------------
-// X phase, relax pass with a depth-1 software pipeline over the warp's tiles:
-// while tile t's distance gathers / relaxes run, the edges of tile t+GW are
-// already in flight and the row data of tile t+2GW is loading.  (The
-// predecessor pass keeps the simpler phase_expand above.)
-// ---------------------------------------------------------------------------
-template <class V, class EI, bool RAW>
-__device__ void phase_relax_pipe(const KParams<V, EI>& P, int p, uint32_t r, bool dense, Smem<V, EI>& s,
-                                 unsigned long long& acc_w, unsigned long long& acc_fd,
-                                 unsigned long long& acc_multi, uint32_t& round_w) {
-  using CD = Codec<V, RAW>;
-  using K = typename CD::K;
-  using WB = typename CD::WB;
-  using C = typename CD::C;
-  const unsigned long long pk = ldcg(&P.st->res[p]);
-  const uint32_t cnt = (uint32_t)pk_count(pk, P.ebits);
-  const EI E = (EI)pk_edges(pk, P.ebits);
-  if (E == 0) return;
-  // Hot-node cache (dense rounds, tuning knob "hot_nodes", off by default):
-  // nodes [0, hot) are read into shared memory when the phase starts, and a
-  // CTA-local running min (ATOMS.MIN) filters candidates already beaten in the
-  // CTA.  The cached value was read during this round, so it is <= the
-  // round-start value and `cand < cached` still proves the node is lowered
-  // this round (the same argument as the L1-cached gathers).
-  const uint32_t hot = dense ? P.hot : 0u;
-  K* hs = reinterpret_cast<K*>(reinterpret_cast<unsigned char*>(&s) + sizeof(Smem<V, EI>));
-  if (hot) {
-    for (uint32_t i = threadIdx.x; i < hot; i += NT) hs[i] = ldcg(P.dist + i);
-    __syncthreads();
-  }
-  const EI T = (E + (EI)(WT - 1)) / (EI)WT;
-  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const EI GW = (EI)gridDim.x * WPB;
-  EI t = (EI)blockIdx.x * WPB + wid;
-  if (t >= T) return;  // warp-uniform; no CTA barrier below
-  WarpRows<V, EI>& w = s.w[wid];
-  const int np = p ^ 1;
-  const int eb = P.ebits;
-  const uint32_t src = P.src;
-  const uint32_t* tile_row = P.tile_row;
-  const EI* qbase = P.qbase[p];
-  const EI* qoff = P.qoff[p];
-  const K* qkey = P.qkey[p];
-  auto row_bound = [&](EI q, uint32_t which) -> uint32_t {
-    const EI x = q + (EI)which;
-    return (x < T) ? ldcg(tile_row + x) : cnt - 1;
-  };
-
-  // rows of tile tt (row i0+lane in lane registers) -> each item's row value and
-  // edge position; then all ITEMS edge loads issued back to back
-  auto stage = [&](EI tt, uint32_t ci0, uint32_t cil, EI c_base, EI c_off, K c_key, uint32_t (&col)[ITEMS],
-                   WB (&wv)[ITEMS], C (&rv)[ITEMS], unsigned& okm) {
-    const EI e0 = tt * (EI)WT;
-    const uint32_t len = (E - e0 < (EI)WT) ? (uint32_t)(E - e0) : (uint32_t)WT;
-    const uint32_t nrows = cil - ci0 + 1;
-    const bool fast = nrows <= 32;
-    const C c_val = CD::dec(c_key);
-    const uint32_t c_rst = (lane < nrows) ? (uint32_t)(c_off > e0 ? c_off - e0 : (EI)0) : 0xFFFFFFFFu;
-    EI pos[ITEMS];
-    if (fast) {
-      uint32_t before = 0;  // rows starting before the current 32-edge window
-#pragma unroll
-      for (int j = 0; j < ITEMS; ++j) {
-        const uint32_t lo = j * 32;
-        const uint32_t bit = (c_rst - lo < 32u) ? (1u << (c_rst - lo)) : 0u;
-        const uint32_t B = __reduce_or_sync(0xffffffffu, bit);
-        const uint32_t k = before + __popc(B & (0xFFFFFFFFu >> (31 - lane))) - 1;
-        before += __popc(B);
-        pos[j] = __shfl_sync(0xffffffffu, c_base, k) + e0 + (EI)(lo + lane);
-        rv[j] = __shfl_sync(0xffffffffu, c_val, k);
-      }
-    } else {
-      // short rows: row-start marks in shared memory + warp max-scan
-      reinterpret_cast<uint4*>(w.mark)[lane] = make_uint4(0, 0, 0, 0);
-      __syncwarp();
-      if (c_rst < len) w.mark[c_rst] = (uint16_t)lane;
-      for (uint32_t k = 32 + lane; k < nrows; k += 32) {
-        const EI off = __ldca(qoff + ci0 + k);
-        const EI rst = off > e0 ? off - e0 : (EI)0;
-        if (rst < (EI)len) w.mark[rst] = (uint16_t)k;
-      }
-      __syncwarp();
-      const uint4 mv = reinterpret_cast<uint4*>(w.mark)[lane];
-      uint32_t m8[8] = {mv.x & 0xFFFFu, mv.x >> 16, mv.y & 0xFFFFu, mv.y >> 16,
-                        mv.z & 0xFFFFu, mv.z >> 16, mv.w & 0xFFFFu, mv.w >> 16};
-      uint32_t run = 0;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) { run = max(run, m8[j]); m8[j] = run; }
-      uint32_t incl = run;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, d);
-        if (lane >= (uint32_t)d) incl = max(incl, y);
-      }
-      uint32_t pre = __shfl_up_sync(0xffffffffu, incl, 1);
-      if (lane == 0) pre = 0;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) m8[j] = max(m8[j], pre);
-      reinterpret_cast<uint4*>(w.mark)[lane] =
-          make_uint4(m8[0] | (m8[1] << 16), m8[2] | (m8[3] << 16), m8[4] | (m8[5] << 16),
-                     m8[6] | (m8[7] << 16));
-      __syncwarp();
-#pragma unroll
-      for (int j = 0; j < ITEMS; ++j) {
-        // queue entries were written before the last grid barrier, whose fence
-        // invalidated L1: L1-cached reads are coherent here
-        const uint32_t k = w.mark[j * 32 + lane];
-        pos[j] = __ldca(qbase + ci0 + k) + e0 + (EI)(j * 32 + lane);
-        rv[j] = CD::dec(__ldca(qkey + ci0 + k));
-      }
-      __syncwarp();  // marks are rewritten by the next stage
-    }
-    okm = 0xFFu;
-    if (len != (uint32_t)WT) {
-      okm = 0;
-#pragma unroll
-      for (int j = 0; j < ITEMS; ++j) okm |= (unsigned)(j * 32 + lane < len) << j;
-    }
-    const EI safe0 = __shfl_sync(0xffffffffu, c_base, 0) + e0;  // the tile's first edge
-#pragma unroll
-    for (int j = 0; j < ITEMS; ++j) EdgeAccess<V>::load(P, ((okm >> j) & 1u) ? pos[j] : safe0, col[j], wv[j]);
-  };
-
-  auto load_rows = [&](uint32_t ci0, uint32_t cil, EI& b, EI& o, K& k) {
-    b = 0;
-    o = 0;
-    k = 0;
-    if (lane <= cil - ci0) {
-      b = ldcg(qbase + ci0 + lane);
-      o = ldcg(qoff + ci0 + lane);
-      k = ldcg(qkey + ci0 + lane);
-    }
-  };
-
-  // ---- prologue: edges of tile t in flight; rows of t+GW loading; range of t+2GW ----
-  uint32_t col[ITEMS];
-  WB wv[ITEMS];
-  C rv[ITEMS];
-  unsigned okm;
-  uint32_t i0, il;
-  EI pf_base, pf_off;
-  K pf_key;
-  {
-    const uint32_t a0 = row_bound(t, 0), a1 = row_bound(t, 1);
-    EI b, o;
-    K k;
-    load_rows(a0, a1, b, o, k);
-    stage(t, a0, a1, b, o, k, col, wv, rv, okm);
-  }
-  i0 = 0;
-  il = 0;
-  pf_base = 0;
-  pf_off = 0;
-  pf_key = 0;
-  if (t + GW < T) {
-    i0 = row_bound(t + GW, 0);
-    il = row_bound(t + GW, 1);
-    load_rows(i0, il, pf_base, pf_off, pf_key);
-  }
-  uint32_t tr = (lane < 2 && t + 2 * GW < T) ? row_bound(t + 2 * GW, lane) : 0u;
-
-  for (; t < T; t += GW) {
-    const EI tn = t + GW;
-    uint32_t ncol[ITEMS];
-    WB nwv[ITEMS];
-    C nrv[ITEMS];
-    unsigned nokm = 0;
-    if (tn < T) {  // warp-uniform
-      stage(tn, i0, il, pf_base, pf_off, pf_key, ncol, nwv, nrv, nokm);
-      const uint32_t ni0 = __shfl_sync(0xffffffffu, tr, 0), nil = __shfl_sync(0xffffffffu, tr, 1);
-      if (tn + GW < T) {
-        i0 = ni0;
-        il = nil;
-        load_rows(i0, il, pf_base, pf_off, pf_key);
-      }
-      tr = (lane < 2 && tn + 2 * GW < T) ? row_bound(tn + 2 * GW, lane) : 0u;
-    }
-    // ---- relax tile t ----
-    unsigned ok = okm;
-    K cand[ITEMS];
-#pragma unroll
-    for (int j = 0; j < ITEMS; ++j) {
-      cand[j] = CD::relax(rv[j], wv[j]);
-      if (!CD::usable(cand[j])) ok &= ~(1u << j);
-    }
-    // read-before-write filter through L1 (see phase_expand for why ld.ca is safe)
-    K cur[ITEMS];
-#pragma unroll
-    for (int j = 0; j < ITEMS; ++j)
-      cur[j] = ((ok >> j) & 1u) ? (col[j] < hot ? hs[col[j]] : __ldca(P.dist + col[j])) : (K)0;
-    unsigned need = 0;
-#pragma unroll
-    for (int j = 0; j < ITEMS; ++j) {
-      if (((ok >> j) & 1u) && cand[j] < cur[j]) {
-        if (col[j] == src) P.st->flag = 1u;  // source guard (solver.py:299-303, :374-376, :236-239)
-        else if (col[j] >= hot || cand[j] < atomicMin(hs + col[j], cand[j])) need |= 1u << j;
-      }
-    }
-    if (need) {
-#pragma unroll
-      for (int j = 0; j < ITEMS; ++j)
-        if ((need >> j) & 1u) atomicMin(P.dist + col[j], cand[j]);
-    }
-    if (dense) {
-      if (need) {
-#pragma unroll
-        for (int j = 0; j < ITEMS; ++j)
-          if ((need >> j) & 1u) P.stamp[col[j]] = r;
-      }
-    } else if (__any_sync(0xffffffffu, need != 0u)) {
-      // sparse: elect one writer per (node, round), enqueue its row
-      unsigned first = 0;
-#pragma unroll
-      for (int j = 0; j < ITEMS; ++j)
-        if (((need >> j) & 1u) && atomicExch(P.stamp + col[j], r) != r) first |= 1u << j;
-      unsigned long long mine = 0;  // (entries << eb) | edges of this lane
-      EI rs[ITEMS], dg[ITEMS];
-#pragma unroll
-      for (int j = 0; j < ITEMS; ++j) {
-        rs[j] = 0;
-        dg[j] = 0;
-        if ((first >> j) & 1u) {
-          round_w++;
-          acc_w++;
-          count_write(P.wstate, col[j], acc_fd, acc_multi);
-          const EI a = __ldg(P.row_ptr + col[j]), b = __ldg(P.row_ptr + col[j] + 1);
-          rs[j] = a;
-          dg[j] = b - a;
-          if (b > a) mine += (1ull << eb) + (unsigned long long)(b - a);  // rows without edges never rescan
-          else first &= ~(1u << j);
-        }
-      }
-      unsigned long long incl = mine;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const unsigned long long y = __shfl_up_sync(0xffffffffu, incl, d);
-        if (lane >= (uint32_t)d) incl += y;
-      }
-      const unsigned long long tot = __shfl_sync(0xffffffffu, incl, 31);
-      if (tot) {
-        unsigned long long base = 0;
-        if (lane == 0) base = atomicAdd(&P.st->res[np], tot);
-        base = __shfl_sync(0xffffffffu, base, 0);
-        const unsigned long long at = base + incl - mine;
-        uint32_t qp = (uint32_t)pk_count(at, eb);
-        EI off = (EI)pk_edges(at, eb);
-#pragma unroll
-        for (int j = 0; j < ITEMS; ++j) {
-          if ((first >> j) & 1u) {
-            P.qnode[np][qp] = col[j];
-            P.qoff[np][qp] = off;
-            P.qbase[np][qp] = rs[j] - off;
-            qp++;
-            off += dg[j];
-          }
-        }
-      }
-    }
-    // ---- rotate the pipeline ----
-#pragma unroll
-    for (int j = 0; j < ITEMS; ++j) {
-      col[j] = ncol[j];
-      wv[j] = nwv[j];
-      rv[j] = nrv[j];
-    }
-    okm = nokm;
-  }
-}
 
 // ---------------------------------------------------------------------------
 // Negative-cycle early exit: a cycle in the predecessor graph (each finite
@@ -898,10 +640,10 @@ __device__ bool pred_graph_has_cycle(const KParams<V, EI>& P) {
 // ---------------------------------------------------------------------------
 // WITH_PRED instantiates the predecessor pass and the negative-cycle check;
 // the plain instance carries none of their registers.
-template <class V, class EI, bool WITH_PRED, bool RAW>
+template <class V, class EI, bool WITH_PRED, bool RAW, int XI>
 __global__ void __launch_bounds__(NT, DAWN_MIN_BLOCKS) dawn_persistent(KParams<V, EI> P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  Smem<V, EI>& s = *reinterpret_cast<Smem<V, EI>*>(smem_raw);
+  Smem<V, EI, XI>& s = *reinterpret_cast<Smem<V, EI, XI>*>(smem_raw);
   DevState* st = P.st;
   const bool leader = (blockIdx.x == 0 && threadIdx.x == 0);
 
@@ -922,11 +664,11 @@ __global__ void __launch_bounds__(NT, DAWN_MIN_BLOCKS) dawn_persistent(KParams<V
       }
       if (r >= 2 && (dense_prev || P.algo == 1)) {
         uint32_t prev_w = 0;
-        phase_compact<V, EI>(P, p, r, s, acc_w, acc_fd, acc_multi, prev_w);
+        phase_compact<V, EI, XI>(P, p, r, s, acc_w, acc_fd, acc_multi, prev_w);
         prev_w = __reduce_add_sync(0xffffffffu, prev_w);
         if ((threadIdx.x & 31) == 0 && prev_w) atomicAdd(&st->wround[p ^ 1], (unsigned long long)prev_w);
       } else {
-        phase_snapshot<V, EI>(P, p);
+        phase_snapshot<V, EI, XI>(P, p);
       }
       grid_sync(&st->bar);
       // ---- termination (solver.py:284-285, :313-317, :356-358, :388-395) ----
@@ -975,13 +717,13 @@ __global__ void __launch_bounds__(NT, DAWN_MIN_BLOCKS) dawn_persistent(KParams<V
       P.prof[4 * r + 3] = ldcg(&st->res[p]);
     }
     uint32_t round_w = 0;
-    phase_relax_pipe<V, EI, RAW>(P, p, r, dense, s, acc_w, acc_fd, acc_multi, round_w);
+    phase_expand<V, EI, false, RAW, XI>(P, p, r, dense, s, acc_w, acc_fd, acc_multi, round_w);
     round_w = __reduce_add_sync(0xffffffffu, round_w);
     if ((threadIdx.x & 31) == 0 && round_w) atomicAdd(&st->wround[p], (unsigned long long)round_w);
     grid_sync(&st->bar);
     if (leader) st->resume_x = 0u;  // every CTA has read it (first barrier passed)
     if constexpr (WITH_PRED) {
-      phase_expand<V, EI, true, RAW>(P, p, r, dense, s, acc_w, acc_fd, acc_multi, round_w);
+      phase_expand<V, EI, true, RAW, XI>(P, p, r, dense, s, acc_w, acc_fd, acc_multi, round_w);
       grid_sync(&st->bar);
     }
     if (prof) P.prof[4 * r + 2] = globaltimer();

@@ -17,7 +17,6 @@ def main():
     ap.add_argument("--scale", type=int, default=22)
     ap.add_argument("--solves", type=int, default=5)
     ap.add_argument("--order", default="indeg")
-    ap.add_argument("--hot", default="0", help="comma list of hot_nodes settings to time on the relabeled graph")
     a = ap.parse_args()
     import numpy as np
     import torch
@@ -32,7 +31,6 @@ def main():
 
     def solve(dg, src, hot=0):
         s = dg.solver(0)
-        N.check(L.dawn_solver_tune(s, b"hot_nodes", float(hot)))
         ts = []
         for _ in range(a.solves):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -76,13 +74,6 @@ def main():
     s1 = int(new_of_old[0])
     t1, d1, st1 = solve(dg1, s1)
     print(f"relabeled: {[round(x, 3) for x in t1]}  R={st1.relaxations}  (source 0 -> {s1})")
-    for h in [int(x) for x in a.hot.split(",") if int(x) > 0]:
-        th, dh, sth = solve(dg1, s1, h)
-        assert torch.equal(dh, d1) and sth.relaxations == st1.relaxations and sth.writes == st1.writes
-        print(f"relabeled hot={h}: {[round(x, 3) for x in th]}")
-        th, dh, sth = solve(dg0, 0, h)
-        assert torch.equal(dh, d0)
-        print(f"original  hot={h}: {[round(x, 3) for x in th]}")
     assert torch.equal(d1[new_of_old], d0), "distances differ after relabeling"
     assert st1.relaxations == st0.relaxations and st1.writes == st0.writes
     top = torch.sort(indeg, descending=True).values
