@@ -487,7 +487,7 @@ def ours(args):
         "config": workload_config(args, {"l2": "flushed between steps (256 MiB write outside the timed events)",
                                          "precision": "fp32 (opt-in, <=1e-6 relative vs the fp64 reference)"}),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "peak_source": peak_src, "kernel": "dawn_persistent<float,uint32>",
+                     "traffic": traffic, "peak_source": peak_src, "kernel": "dawn_persistent<float,uint32,wide>",
                      "bytes_alg": b_alg, "kernel_ms": 1e3 * t_kern,
                      "bytes_formula": "12*R + 16*(W+1) + 12*W (col+w+dist per relax; row_ptr+frontier per scan; "
                                       "dist+frontier per write)"},
