@@ -116,7 +116,10 @@ int dawn_solver_destroy(dawn_solver_t s);
  *   "batch_min_sources" (default 4): dawn_mssp batches k >= value sources.
  *   "wide_tiles" (default -1 = auto): 1 / 0 forces wide (14 edges per lane)
  *   or narrow (8) X-phase warp tiles for 4-byte values; auto = wide when
- *   m >= 2^25 and m >= 8n. */
+ *   m >= 2^25 and m >= 8n.
+ *   "bitmap_frontier" (default -1 = auto): 1 / 0 forces / disables the
+ *   bitmap frontier of light rounds (auto: average out-degree < 8 and
+ *   n >= 4096, narrow tiles; never with predecessors). */
 int dawn_solver_tune(dawn_solver_t s, const char* key, double value);
 
 /* One single-source solve: govm_sssp / gsvm_sssp (solver.py:265-399),

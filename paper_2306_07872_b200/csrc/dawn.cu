@@ -77,6 +77,7 @@ struct dawn_solver_s {
   unsigned flags = 0;
   void* dist = nullptr;
   uint32_t* stamp = nullptr;
+  uint32_t* bmap = nullptr;      // bitmap frontier (low-degree graphs)
   uint8_t* wstate = nullptr;
   unsigned long long* pred = nullptr;
   uint32_t* jmp0 = nullptr;
@@ -98,6 +99,8 @@ struct dawn_solver_s {
   double dense_edges_per_node = 0.5;
   int wide_pref = -1;                 // tunable "wide_tiles": -1 auto, 0 narrow, 1 wide X-phase tiles
   bool wide = false;
+  int fb_pref = -1;                   // tunable "bitmap_frontier": -1 auto, 0 off, 1 on
+  bool fb = false;
   double batch_min_sources = 4;       // tunable: dawn_mssp batches when k >= this  // tunable: dense frontier build after rounds relaxing >= this * n edges
   int ebits = 32;
   int logn = 0;
@@ -421,6 +424,7 @@ struct Impl {
     P.ew = g->ew;
     P.dist = (K*)s->dist;
     P.stamp = s->stamp;
+    P.bmap = s->bmap;
     P.wstate = s->wstate;
     P.pred = s->pred;
     P.jmp0 = s->jmp0;
@@ -457,6 +461,9 @@ struct Impl {
   }
   static void* kernel_for(dawn_solver_t s, bool pred) {
     const bool raw = !s->g->has_negative;
+    if (!pred && s->fb)  // bitmap-frontier variant (narrow tiles, no predecessor pass)
+      return raw ? (void*)dawn_persistent<V, EI, false, true, XI_NARROW, true>
+                 : (void*)dawn_persistent<V, EI, false, false, XI_NARROW, true>;
     return s->wide ? kernel<XW>(pred, raw) : kernel<XI_NARROW>(pred, raw);
   }
 
@@ -464,9 +471,18 @@ struct Impl {
     const int64_t n = s->g->n, m = s->g->m;
     if (s->wide_pref < 0) s->wide = XW != XI_NARROW && m >= (1ll << 25) && m >= 8 * n;
     else s->wide = XW != XI_NARROW && s->wide_pref > 0;
+    // low-degree graphs (average out-degree < 8, e.g. grids / road networks):
+    // light rounds keep a bitmap frontier instead of enqueueing every write
+    if (s->fb_pref < 0) s->fb = !s->wide && m < 8 * n && n >= 4096;
+    else s->fb = !s->wide && s->fb_pref > 0;
     const size_t sm = s->wide ? sizeof(Smem<V, EI, XW>) : sizeof(Smem<V, EI, XI_NARROW>);
     const void* k0 = kernel_for(s, false);
     const void* k1 = kernel_for(s, true);
+    if (s->fb) {  // the predecessor-tracking instance stays on the queue frontier
+      const bool raw = !s->g->has_negative;
+      const void* kq = s->wide ? kernel<XW>(false, raw) : kernel<XI_NARROW>(false, raw);
+      CK(cudaFuncSetAttribute(kq, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    }
     CK(cudaFuncSetAttribute(k0, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     CK(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     // Keep the shared-memory carveout to what DAWN_MIN_BLOCKS resident CTAs
@@ -495,6 +511,7 @@ struct Impl {
     const int64_t n = s->g->n;
     CK(cudaMemsetAsync(s->dist, 0xFF, sizeof(K) * n, stream));
     CK(cudaMemsetAsync(s->stamp, 0, sizeof(uint32_t) * n, stream));
+    CK(cudaMemsetAsync(s->bmap, 0, 4 * (size_t)((n + 31) / 32 + 4), stream));
     CK(cudaMemsetAsync(s->wstate, 0, (size_t)n, stream));
     if (s->prof) CK(cudaMemsetAsync(s->prof, 0, 32 * (size_t)s->prof_cap, stream));
     if (s->pred) CK(cudaMemsetAsync(s->pred, 0, sizeof(unsigned long long) * n, stream));
@@ -651,6 +668,7 @@ struct Impl {
     const size_t ks = sizeof(K), es = sizeof(EI);
     CK(cudaMalloc(&s->dist, ks * n));
     CK(cudaMalloc(&s->stamp, 4 * n));
+    CK(cudaMalloc(&s->bmap, 4 * (size_t)((n + 31) / 32 + 4)));  // padded for 16-byte loads
     CK(cudaMalloc(&s->wstate, (size_t)n));
     if (s->flags & (DAWN_F_PRED | DAWN_F_NEGCHECK)) {
       CK(cudaMalloc(&s->pred, 8 * n));
@@ -696,6 +714,7 @@ static void solver_free(dawn_solver_t s) {
   cudaSetDevice(s->g->device);
   cudaFree(s->dist);
   cudaFree(s->stamp);
+  cudaFree(s->bmap);
   cudaFree(s->wstate);
   cudaFree(s->pred);
   cudaFree(s->jmp0);
@@ -756,6 +775,12 @@ extern "C" int dawn_solver_tune(dawn_solver_t s, const char* key, double value) 
   if (!strcmp(key, "wide_tiles")) {
     if (!(value == -1.0 || value == 0.0 || value == 1.0)) return fail(DAWN_EINVAL, "wide_tiles must be -1, 0 or 1");
     s->wide_pref = (int)value;
+    CK(cudaSetDevice(s->g->device));
+    return DISPATCH(s->g, setup(s));
+  }
+  if (!strcmp(key, "bitmap_frontier")) {
+    if (!(value == -1.0 || value == 0.0 || value == 1.0)) return fail(DAWN_EINVAL, "bitmap_frontier must be -1, 0 or 1");
+    s->fb_pref = (int)value;
     CK(cudaSetDevice(s->g->device));
     return DISPATCH(s->g, setup(s));
   }

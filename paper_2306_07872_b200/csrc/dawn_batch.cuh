@@ -399,7 +399,10 @@ __device__ void bphase_expand(const BParams<V, EI>& P, uint32_t r, const uint32_
   constexpr int LPT = BLanes<V>::LPT, TPE = BLanes<V>::TPE, EPW = BLanes<V>::EPW;
   constexpr uint32_t LMASK = BLanes<V>::LMASK;
   constexpr int STEPS = 32 / EPW;               // warp steps per tile
-  constexpr int U = sizeof(K) == 4 ? 4 : 2;     // steps in flight
+#ifndef DAWN_BATCH_U
+#define DAWN_BATCH_U 4
+#endif
+  constexpr int U = sizeof(K) == 4 ? DAWN_BATCH_U : 2;  // steps in flight
   // a candidate is usable iff it is below +inf: clamp the current value there,
   // so `cand < min(cur, +inf)` is the reference's `alpha[idx] > cand` with an
   // infinite candidate never written (solver.py:298, :373)

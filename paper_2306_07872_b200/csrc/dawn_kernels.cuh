@@ -45,6 +45,7 @@ struct KParams {
   const unsigned long long* ew;        // SoA weights for 8-byte value types
   K* dist;
   uint32_t* stamp;                     // last round that lowered the node (0 = never)
+  uint32_t* bmap;                      // bitmap-frontier kernels: nodes lowered in a light round, 1 bit each
   uint8_t* wstate;                     // 0 never lowered, 1 lowered in one round, 2 in >= 2
   unsigned long long* pred;            // (round << 32) | ~u, or nullptr
   uint32_t* jmp0;
@@ -322,6 +323,136 @@ __device__ void phase_compact(const KParams<V, EI>& P, int p, uint32_t r, Smem<V
 }
 
 // ---------------------------------------------------------------------------
+// S phase after a light round, bitmap-frontier kernels (low-degree graphs such
+// as the grid, where a light round lowers ~25% of the nodes it touches and the
+// enqueue path's election + reservation chain per write dominates).  A warp
+// takes 128 bitmap words (4096 nodes), spreads their set bits evenly over its
+// lanes (popc prefix + per-lane search + __fns), does the write bookkeeping,
+// sizes its entries, reserves them with ONE atomic and writes them (a second
+// pass re-derives the same slots; the first two slots per lane are kept).
+// ---------------------------------------------------------------------------
+template <class V, class EI, int XI>
+__device__ void phase_bitmap(const KParams<V, EI>& P, int p, uint32_t r, unsigned long long& acc_w,
+                             unsigned long long& acc_fd, unsigned long long& acc_multi, uint32_t& prev_w) {
+  constexpr uint32_t WPL = 4;        // bitmap words per lane (one 16-byte load)
+  constexpr uint32_t CW = 32 * WPL;  // words per warp chunk
+  const uint32_t n = P.n;
+  const uint32_t nwords = (n + 31u) >> 5;
+  const uint32_t nchunks = (nwords + CW - 1) / CW;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t nwarps = gridDim.x * (NT / 32);
+  const int eb = P.ebits;
+  auto load_words = [&](uint32_t c, uint4& w4) {
+    const uint32_t w0 = c * CW + lane * WPL;
+    if (w0 + WPL <= nwords) {
+      w4 = __ldcg(reinterpret_cast<const uint4*>(P.bmap + w0));
+    } else {
+      w4.x = (w0 + 0 < nwords) ? ldcg(P.bmap + w0 + 0) : 0u;
+      w4.y = (w0 + 1 < nwords) ? ldcg(P.bmap + w0 + 1) : 0u;
+      w4.z = (w0 + 2 < nwords) ? ldcg(P.bmap + w0 + 2) : 0u;
+      w4.w = (w0 + 3 < nwords) ? ldcg(P.bmap + w0 + 3) : 0u;
+    }
+  };
+  uint32_t c = blockIdx.x * (NT / 32) + (threadIdx.x >> 5);
+  uint4 nxt = make_uint4(0, 0, 0, 0);
+  if (c < nchunks) load_words(c, nxt);
+  for (; c < nchunks; c += nwarps) {
+    const uint4 w4 = nxt;
+    if (c + nwarps < nchunks) load_words(c + nwarps, nxt);  // prefetch the next chunk
+    const uint32_t any = w4.x | w4.y | w4.z | w4.w;
+    if (!__any_sync(0xffffffffu, any != 0u)) continue;
+    const uint32_t w0 = c * CW + lane * WPL;
+    if (any) {  // consumed: the next light round sets bits again
+      if (w0 + WPL <= nwords) *reinterpret_cast<uint4*>(P.bmap + w0) = make_uint4(0, 0, 0, 0);
+      else
+        for (uint32_t q = 0; q < WPL; ++q)
+          if (w0 + q < nwords) P.bmap[w0 + q] = 0u;
+    }
+    const uint32_t pc = __popc(w4.x) + __popc(w4.y) + __popc(w4.z) + __popc(w4.w);
+    uint32_t incl = pc;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= (uint32_t)d) incl += y;
+    }
+    const uint32_t excl = incl - pc;
+    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+    auto slot_node = [&](uint32_t sl) -> uint32_t {
+      uint32_t lo = 0;
+#pragma unroll
+      for (int step = 16; step > 0; step >>= 1) {
+        const uint32_t x = __shfl_sync(0xffffffffu, excl, (lo + step) & 31);
+        if (lo + step < 32u && x <= sl) lo += step;
+      }
+      uint32_t k = sl - __shfl_sync(0xffffffffu, excl, lo);
+      const uint32_t a0 = __shfl_sync(0xffffffffu, w4.x, lo), a1 = __shfl_sync(0xffffffffu, w4.y, lo);
+      const uint32_t a2 = __shfl_sync(0xffffffffu, w4.z, lo), a3 = __shfl_sync(0xffffffffu, w4.w, lo);
+      uint32_t wd = a0, q = 0;
+      const uint32_t c0 = __popc(a0), c1 = __popc(a1), c2 = __popc(a2);
+      if (k >= c0) { k -= c0; wd = a1; q = 1; if (k >= c1) { k -= c1; wd = a2; q = 2; if (k >= c2) { k -= c2; wd = a3; q = 3; } } }
+      return ((c * CW + lo * WPL + q) << 5) + (uint32_t)__fns(wd, 0, (int)k + 1);
+    };
+    // ---- pass A: bookkeeping of round r-1's writes; size this lane's entries ----
+    unsigned long long mine = 0;  // (entries << eb) | edges
+    uint32_t kv[2] = {0, 0};
+    EI ka[2] = {0, 0}, kb[2] = {0, 0};
+    for (uint32_t s0 = 0, it = 0; s0 < total; s0 += 32, ++it) {
+      const uint32_t sl = s0 + lane;
+      const uint32_t v = slot_node(sl < total ? sl : total - 1);
+      if (sl < total) {
+        const uint8_t ws = ldcg(P.wstate + v);
+        const EI a = __ldg(P.row_ptr + v), b = __ldg(P.row_ptr + v + 1);
+        prev_w++;
+        acc_w++;
+        if (ws == 0) { acc_fd++; P.wstate[v] = 1; }
+        else if (ws == 1) { acc_multi++; P.wstate[v] = 2; }
+        P.stamp[v] = r - 1;
+        if (b > a) mine += (1ull << eb) + (unsigned long long)(b - a);  // rows without edges never rescan
+        if (it < 2) { kv[it] = v; ka[it] = a; kb[it] = b; }
+      }
+    }
+    unsigned long long pre = mine;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const unsigned long long y = __shfl_up_sync(0xffffffffu, pre, d);
+      if (lane >= (uint32_t)d) pre += y;
+    }
+    const unsigned long long tot = __shfl_sync(0xffffffffu, pre, 31);
+    if (tot == 0ull) continue;
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(&P.st->res[p], tot);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    const unsigned long long at = base + pre - mine;
+    uint32_t pos = (uint32_t)pk_count(at, eb);
+    EI off = (EI)pk_edges(at, eb);
+    // ---- pass B: write the entries (the same slots in the same order) ----
+    for (uint32_t s0 = 0, it = 0; s0 < total; s0 += 32, ++it) {
+      const uint32_t sl = s0 + lane;
+      uint32_t v;
+      EI a, b;
+      if (it < 2) {
+        v = kv[it & 1];
+        a = ka[it & 1];
+        b = kb[it & 1];
+      } else {
+        v = slot_node(sl < total ? sl : total - 1);
+        a = __ldg(P.row_ptr + v);
+        b = __ldg(P.row_ptr + v + 1);
+      }
+      if (sl < total && b > a) {
+        P.qnode[p][pos] = v;
+        P.qoff[p][pos] = off;
+        P.qbase[p][pos] = a - off;
+        P.qkey[p][pos] = ldcg(P.dist + v);
+        mark_tiles<XI, EI>(P.tile_row, off, b - a, pos);
+        pos++;
+        off += b - a;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // X phase: warp tiles of the frontier's virtual edge list.
 //   PRED == false : relax (+ enqueue when !dense)
 //   PRED == true  : predecessor pass — among this round's frontier edges that
@@ -339,7 +470,7 @@ __device__ void phase_compact(const KParams<V, EI>& P, int p, uint32_t r, Smem<V
 // ---------------------------------------------------------------------------
 constexpr uint32_t SENT = 0xFFFFFFFFu;
 
-template <class V, class EI, bool PRED, bool RAW, int XI>
+template <class V, class EI, bool PRED, bool RAW, int XI, bool FB = false>
 __device__ void phase_expand(const KParams<V, EI>& P, int p, uint32_t r, bool dense, Smem<V, EI, XI>& s,
                              unsigned long long& acc_w, unsigned long long& acc_fd,
                              unsigned long long& acc_multi, uint32_t& round_w) {
@@ -526,6 +657,13 @@ __device__ void phase_expand(const KParams<V, EI>& P, int p, uint32_t r, bool de
           for (int j = 0; j < XI; ++j)
             if ((need >> j) & 1u) P.stamp[col[j]] = r;
         }
+      } else if constexpr (FB) {
+        // ---- light round, bitmap frontier: one bit per lowered node (red.or) ----
+        if (need) {
+#pragma unroll
+          for (int j = 0; j < XI; ++j)
+            if ((need >> j) & 1u) atomicOr(P.bmap + (col[j] >> 5), 1u << (col[j] & 31u));
+        }
       } else if (__any_sync(0xffffffffu, need != 0u)) {
         // ---- sparse: elect one writer per (node, round), enqueue its row ----
         unsigned first = 0;
@@ -640,7 +778,9 @@ __device__ bool pred_graph_has_cycle(const KParams<V, EI>& P) {
 // ---------------------------------------------------------------------------
 // WITH_PRED instantiates the predecessor pass and the negative-cycle check;
 // the plain instance carries none of their registers.
-template <class V, class EI, bool WITH_PRED, bool RAW, int XI>
+// FB: light rounds record their writes in a bitmap (low-degree graphs) instead
+// of enqueueing them; never combined with WITH_PRED.
+template <class V, class EI, bool WITH_PRED, bool RAW, int XI, bool FB = false>
 __global__ void __launch_bounds__(NT, DAWN_MIN_BLOCKS) dawn_persistent(KParams<V, EI> P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem<V, EI, XI>& s = *reinterpret_cast<Smem<V, EI, XI>*>(smem_raw);
@@ -665,6 +805,11 @@ __global__ void __launch_bounds__(NT, DAWN_MIN_BLOCKS) dawn_persistent(KParams<V
       if (r >= 2 && (dense_prev || P.algo == 1)) {
         uint32_t prev_w = 0;
         phase_compact<V, EI, XI>(P, p, r, s, acc_w, acc_fd, acc_multi, prev_w);
+        prev_w = __reduce_add_sync(0xffffffffu, prev_w);
+        if ((threadIdx.x & 31) == 0 && prev_w) atomicAdd(&st->wround[p ^ 1], (unsigned long long)prev_w);
+      } else if (FB && r >= 2) {
+        uint32_t prev_w = 0;
+        phase_bitmap<V, EI, XI>(P, p, r, acc_w, acc_fd, acc_multi, prev_w);
         prev_w = __reduce_add_sync(0xffffffffu, prev_w);
         if ((threadIdx.x & 31) == 0 && prev_w) atomicAdd(&st->wround[p ^ 1], (unsigned long long)prev_w);
       } else {
@@ -717,7 +862,7 @@ __global__ void __launch_bounds__(NT, DAWN_MIN_BLOCKS) dawn_persistent(KParams<V
       P.prof[4 * r + 3] = ldcg(&st->res[p]);
     }
     uint32_t round_w = 0;
-    phase_expand<V, EI, false, RAW, XI>(P, p, r, dense, s, acc_w, acc_fd, acc_multi, round_w);
+    phase_expand<V, EI, false, RAW, XI, FB>(P, p, r, dense, s, acc_w, acc_fd, acc_multi, round_w);
     round_w = __reduce_add_sync(0xffffffffu, round_w);
     if ((threadIdx.x & 31) == 0 && round_w) atomicAdd(&st->wround[p], (unsigned long long)round_w);
     grid_sync(&st->bar);
