@@ -334,6 +334,7 @@ __device__ void phase_compact(const KParams<V, EI>& P, int p, uint32_t r, Smem<V
 template <class V, class EI, int XI>
 __device__ void phase_bitmap(const KParams<V, EI>& P, int p, uint32_t r, unsigned long long& acc_w,
                              unsigned long long& acc_fd, unsigned long long& acc_multi, uint32_t& prev_w) {
+  using K = typename Val<V>::K;
   constexpr uint32_t WPL = 4;        // bitmap words per lane (one 16-byte load)
   constexpr uint32_t CW = 32 * WPL;  // words per warp chunk
   const uint32_t n = P.n;
@@ -392,23 +393,40 @@ __device__ void phase_bitmap(const KParams<V, EI>& P, int p, uint32_t r, unsigne
       if (k >= c0) { k -= c0; wd = a1; q = 1; if (k >= c1) { k -= c1; wd = a2; q = 2; if (k >= c2) { k -= c2; wd = a3; q = 3; } } }
       return ((c * CW + lo * WPL + q) << 5) + (uint32_t)__fns(wd, 0, (int)k + 1);
     };
-    // ---- pass A: bookkeeping of round r-1's writes; size this lane's entries ----
+    // ---- pass A: bookkeeping of round r-1's writes; size this lane's entries.
+    // Two slots per lane per iteration (more loads in flight); the first
+    // iteration's slots are kept for pass B. ----
     unsigned long long mine = 0;  // (entries << eb) | edges
     uint32_t kv[2] = {0, 0};
     EI ka[2] = {0, 0}, kb[2] = {0, 0};
-    for (uint32_t s0 = 0, it = 0; s0 < total; s0 += 32, ++it) {
-      const uint32_t sl = s0 + lane;
-      const uint32_t v = slot_node(sl < total ? sl : total - 1);
-      if (sl < total) {
-        const uint8_t ws = ldcg(P.wstate + v);
-        const EI a = __ldg(P.row_ptr + v), b = __ldg(P.row_ptr + v + 1);
-        prev_w++;
-        acc_w++;
-        if (ws == 0) { acc_fd++; P.wstate[v] = 1; }
-        else if (ws == 1) { acc_multi++; P.wstate[v] = 2; }
-        P.stamp[v] = r - 1;
-        if (b > a) mine += (1ull << eb) + (unsigned long long)(b - a);  // rows without edges never rescan
-        if (it < 2) { kv[it] = v; ka[it] = a; kb[it] = b; }
+    for (uint32_t s0 = 0, it = 0; s0 < total; s0 += 64, ++it) {
+      uint32_t vv[2];
+      EI aa[2], bb[2];
+      uint8_t ww[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const uint32_t sl = s0 + 32 * h + lane;
+        vv[h] = slot_node(sl < total ? sl : total - 1);
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        ww[h] = ldcg(P.wstate + vv[h]);
+        aa[h] = __ldg(P.row_ptr + vv[h]);
+        bb[h] = __ldg(P.row_ptr + vv[h] + 1);
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const uint32_t sl = s0 + 32 * h + lane;
+        if (sl < total) {
+          const uint32_t v = vv[h];
+          prev_w++;
+          acc_w++;
+          if (ww[h] == 0) { acc_fd++; P.wstate[v] = 1; }
+          else if (ww[h] == 1) { acc_multi++; P.wstate[v] = 2; }
+          P.stamp[v] = r - 1;
+          if (bb[h] > aa[h]) mine += (1ull << eb) + (unsigned long long)(bb[h] - aa[h]);
+          if (it == 0) { kv[h] = v; ka[h] = aa[h]; kb[h] = bb[h]; }
+        }
       }
     }
     unsigned long long pre = mine;
@@ -426,27 +444,36 @@ __device__ void phase_bitmap(const KParams<V, EI>& P, int p, uint32_t r, unsigne
     uint32_t pos = (uint32_t)pk_count(at, eb);
     EI off = (EI)pk_edges(at, eb);
     // ---- pass B: write the entries (the same slots in the same order) ----
-    for (uint32_t s0 = 0, it = 0; s0 < total; s0 += 32, ++it) {
-      const uint32_t sl = s0 + lane;
-      uint32_t v;
-      EI a, b;
-      if (it < 2) {
-        v = kv[it & 1];
-        a = ka[it & 1];
-        b = kb[it & 1];
-      } else {
-        v = slot_node(sl < total ? sl : total - 1);
-        a = __ldg(P.row_ptr + v);
-        b = __ldg(P.row_ptr + v + 1);
+    for (uint32_t s0 = 0, it = 0; s0 < total; s0 += 64, ++it) {
+      uint32_t vv[2];
+      EI aa[2], bb[2];
+      K kk[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const uint32_t sl = s0 + 32 * h + lane;
+        if (it == 0) {
+          vv[h] = kv[h];
+          aa[h] = ka[h];
+          bb[h] = kb[h];
+        } else {
+          vv[h] = slot_node(sl < total ? sl : total - 1);
+          aa[h] = __ldg(P.row_ptr + vv[h]);
+          bb[h] = __ldg(P.row_ptr + vv[h] + 1);
+        }
+        kk[h] = ldcg(P.dist + vv[h]);
       }
-      if (sl < total && b > a) {
-        P.qnode[p][pos] = v;
-        P.qoff[p][pos] = off;
-        P.qbase[p][pos] = a - off;
-        P.qkey[p][pos] = ldcg(P.dist + v);
-        mark_tiles<XI, EI>(P.tile_row, off, b - a, pos);
-        pos++;
-        off += b - a;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const uint32_t sl = s0 + 32 * h + lane;
+        if (sl < total && bb[h] > aa[h]) {
+          P.qnode[p][pos] = vv[h];
+          P.qoff[p][pos] = off;
+          P.qbase[p][pos] = aa[h] - off;
+          P.qkey[p][pos] = kk[h];
+          mark_tiles<XI, EI>(P.tile_row, off, bb[h] - aa[h], pos);
+          pos++;
+          off += bb[h] - aa[h];
+        }
       }
     }
   }
