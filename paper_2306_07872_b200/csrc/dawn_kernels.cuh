@@ -331,10 +331,14 @@ __device__ void phase_compact(const KParams<V, EI>& P, int p, uint32_t r, Smem<V
 // sizes its entries, reserves them with ONE atomic and writes them (a second
 // pass re-derives the same slots; the first two slots per lane are kept).
 // ---------------------------------------------------------------------------
+#ifndef DAWN_BITMAP_SLOTS
+#define DAWN_BITMAP_SLOTS 2
+#endif
 template <class V, class EI, int XI>
 __device__ void phase_bitmap(const KParams<V, EI>& P, int p, uint32_t r, unsigned long long& acc_w,
                              unsigned long long& acc_fd, unsigned long long& acc_multi, uint32_t& prev_w) {
   using K = typename Val<V>::K;
+  constexpr int SL = DAWN_BITMAP_SLOTS;  // slots per lane per iteration
   constexpr uint32_t WPL = 4;        // bitmap words per lane (one 16-byte load)
   constexpr uint32_t CW = 32 * WPL;  // words per warp chunk
   const uint32_t n = P.n;
@@ -397,25 +401,27 @@ __device__ void phase_bitmap(const KParams<V, EI>& P, int p, uint32_t r, unsigne
     // Two slots per lane per iteration (more loads in flight); the first
     // iteration's slots are kept for pass B. ----
     unsigned long long mine = 0;  // (entries << eb) | edges
-    uint32_t kv[2] = {0, 0};
-    EI ka[2] = {0, 0}, kb[2] = {0, 0};
-    for (uint32_t s0 = 0, it = 0; s0 < total; s0 += 64, ++it) {
-      uint32_t vv[2];
-      EI aa[2], bb[2];
-      uint8_t ww[2];
+    uint32_t kv[SL];
+    EI ka[SL], kb[SL];
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
+    for (int h = 0; h < SL; ++h) { kv[h] = 0; ka[h] = 0; kb[h] = 0; }
+    for (uint32_t s0 = 0, it = 0; s0 < total; s0 += 32 * SL, ++it) {
+      uint32_t vv[SL];
+      EI aa[SL], bb[SL];
+      uint8_t ww[SL];
+#pragma unroll
+      for (int h = 0; h < SL; ++h) {
         const uint32_t sl = s0 + 32 * h + lane;
         vv[h] = slot_node(sl < total ? sl : total - 1);
       }
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
+      for (int h = 0; h < SL; ++h) {
         ww[h] = ldcg(P.wstate + vv[h]);
         aa[h] = __ldg(P.row_ptr + vv[h]);
         bb[h] = __ldg(P.row_ptr + vv[h] + 1);
       }
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
+      for (int h = 0; h < SL; ++h) {
         const uint32_t sl = s0 + 32 * h + lane;
         if (sl < total) {
           const uint32_t v = vv[h];
@@ -444,12 +450,12 @@ __device__ void phase_bitmap(const KParams<V, EI>& P, int p, uint32_t r, unsigne
     uint32_t pos = (uint32_t)pk_count(at, eb);
     EI off = (EI)pk_edges(at, eb);
     // ---- pass B: write the entries (the same slots in the same order) ----
-    for (uint32_t s0 = 0, it = 0; s0 < total; s0 += 64, ++it) {
-      uint32_t vv[2];
-      EI aa[2], bb[2];
-      K kk[2];
+    for (uint32_t s0 = 0, it = 0; s0 < total; s0 += 32 * SL, ++it) {
+      uint32_t vv[SL];
+      EI aa[SL], bb[SL];
+      K kk[SL];
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
+      for (int h = 0; h < SL; ++h) {
         const uint32_t sl = s0 + 32 * h + lane;
         if (it == 0) {
           vv[h] = kv[h];
@@ -463,7 +469,7 @@ __device__ void phase_bitmap(const KParams<V, EI>& P, int p, uint32_t r, unsigne
         kk[h] = ldcg(P.dist + vv[h]);
       }
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
+      for (int h = 0; h < SL; ++h) {
         const uint32_t sl = s0 + 32 * h + lane;
         if (sl < total && bb[h] > aa[h]) {
           P.qnode[p][pos] = vv[h];
