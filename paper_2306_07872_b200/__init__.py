@@ -33,6 +33,8 @@ from .solver import (
     seed_source,
 )
 
+from .experiments import MuReport, run_mu_experiment
+
 __version__ = "0.1.0"
 
 __all__ = [
@@ -63,4 +65,6 @@ __all__ = [
     "set_default_precision",
     "get_default_precision",
     "set_tuning",
+    "MuReport",
+    "run_mu_experiment",
 ]

@@ -197,11 +197,17 @@ def generate_random_graph(n: int, avg_degree: float, mode: WeightMode, seed: int
         k = int(rng.binomial(n - 1, p)) if n > 1 else 0
         if k == 0:
             continue
-        # k distinct targets among the n-1 non-self slots
-        slots = np.sort(rng.choice(n - 1, size=k, replace=False))
-        tgt = slots + (slots >= u)
+        # k distinct targets among the n-1 non-self slots, drawn exactly as the
+        # reference does (graph.py:433-443): batches of 2*(missing) uniform
+        # slot draws until k distinct ones are in; the set is sorted
+        chosen: set[int] = set()
+        while len(chosen) < k:
+            for t in rng.integers(0, n - 1, size=2 * (k - len(chosen))).tolist():
+                chosen.add(t + 1 if t >= u else t)
+                if len(chosen) == k:
+                    break
         us.append(np.full(k, u, np.int64))
-        vs.append(tgt.astype(np.int64))
+        vs.append(np.array(sorted(chosen), dtype=np.int64))
     if us:
         u_arr, v_arr = np.concatenate(us), np.concatenate(vs)
     else:
