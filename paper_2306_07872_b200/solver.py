@@ -429,6 +429,10 @@ def apsp(g, algo: str = "govm", workers: int = 1, sink: Callable[[DistanceVector
 
     Rows are produced in device batches and handed to ``sink`` strictly in
     source order; the n x n matrix is never held.  A sink exception aborts.
+    On one GPU the row path is pipelined: the device solves
+    tile i+1 (batched kernel, float64 rows into pinned host memory) while a
+    consumer thread hands tile i's rows to ``sink``; two pinned buffers
+    alternate.
     """
     name = _normalize_algo(algo)
     if workers < 1:
@@ -438,11 +442,70 @@ def apsp(g, algo: str = "govm", workers: int = 1, sink: Callable[[DistanceVector
     if n == 0:
         return agg.finish()
     batch = max(1, min(n, (256 << 20) // (8 * n)))
-    for lo in range(0, n, batch):
-        for dv, st in mssp(g, range(lo, min(n, lo + batch)), name, workers, precision=precision):
-            if sink is not None:
-                sink(dv)
-            agg.add(st)
+    if workers > 1 and N.device_count() > 1:
+        for lo in range(0, n, batch):
+            for dv, st in mssp(g, range(lo, min(n, lo + batch)), name, workers, precision=precision):
+                if sink is not None:
+                    sink(dv)
+                agg.add(st)
+        return agg.finish()
+    return _apsp_pipelined(g, name, sink, precision, batch, agg)
+
+
+def _apsp_pipelined(g, name: str, sink, precision, batch: int, agg: AggregateStats) -> AggregateStats:
+    import queue
+
+    import torch
+
+    dg = device_graph(g, precision=precision)
+    n = dg.n
+    algo_id = _ALGO[name]
+    flags = _neg_flags(dg)
+    bufs = [torch.empty((batch, n), dtype=torch.float64).pin_memory() for _ in range(2)]
+    free: "queue.Queue[int]" = queue.Queue()
+    for i in range(2):
+        free.put(i)
+    ready: "queue.Queue" = queue.Queue()
+    failure: list[BaseException] = []
+
+    def consume():
+        while True:
+            item = ready.get()
+            if item is None:
+                return
+            slot, lo, k, stats = item
+            try:
+                if not failure:
+                    rows = np.array(bufs[slot][:k].numpy())  # fresh arrays: the buffer is reused
+                    for i in range(k):
+                        if sink is not None:
+                            sink(DistanceVector(dist=rows[i], source=lo + i))
+                        agg.add(_stats_from_native(stats[i]))
+            except BaseException as e:  # a sink exception aborts apsp (solver.py:470-471)
+                failure.append(e)
+            finally:
+                free.put(slot)
+
+    worker = threading.Thread(target=consume, daemon=True)
+    worker.start()
+    try:
+        with dg.lock:
+            s = dg.solver(flags)
+            for lo in range(0, n, batch):
+                slot = free.get()
+                if failure:
+                    break
+                k = min(batch, n - lo)
+                srcs = np.arange(lo, lo + k, dtype=np.int64)
+                stats = (N.Stats * k)()
+                N.check(N.lib().dawn_mssp(s, srcs.ctypes.data, k, algo_id, flags, bufs[slot].data_ptr(),
+                                          ctypes.addressof(stats), dg.stream()))
+                ready.put((slot, lo, k, stats))
+    finally:
+        ready.put(None)
+        worker.join()
+    if failure:
+        raise failure[0]
     return agg.finish()
 
 
