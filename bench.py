@@ -49,6 +49,9 @@ def parse():
     ap.add_argument("--no-apsp", action="store_true", help="skip the config-3 multi-source leg")
     ap.add_argument("--apsp-sources", type=int, default=8192)
     ap.add_argument("--apsp-scale", type=int, default=20)
+    ap.add_argument("--dist-backend", default="nccl", help="process-group backend (gloo only for the 1-GPU "
+                    "rehearsal of the multi-rank path)")
+    ap.add_argument("--device-map", default=None, help="testing: comma list rank->device (e.g. '0' = all on cuda:0)")
     return ap.parse_args()
 
 
@@ -310,9 +313,16 @@ def ours(args):
     import torch.distributed as dist
 
     rank, world, local = dist_env()
+    if args.device_map:
+        dm = [int(x) for x in args.device_map.split(",")]
+        local = dm[local % len(dm)]
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(args.dist_backend)
+    red_dev = torch.device("cuda", local) if args.dist_backend == "nccl" else torch.device("cpu")
 
     from paper_2306_07872_b200 import build as B
 
@@ -373,7 +383,7 @@ def ours(args):
     kern_ms = [b.elapsed_time(c) for a, b, c in ev]
     tot_ms = sum(step_ms)
     if world > 1:
-        t = torch.tensor([tot_ms], device=dev, dtype=torch.float64)
+        t = torch.tensor([tot_ms], device=red_dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         tot_ms = float(t.item())
 
@@ -438,7 +448,7 @@ def ours(args):
         torch.cuda.synchronize()
         t_e2e = (time.perf_counter() - t0) / KE
         if world > 1:
-            tt = torch.tensor([t_e2e], device=dev, dtype=torch.float64)
+            tt = torch.tensor([t_e2e], device=red_dev, dtype=torch.float64)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             t_e2e = float(tt.item())
         h2d = 8 * (n + 1) + 16 * m_edges

@@ -177,7 +177,7 @@ def apsp_sharded(g, sources: Sequence[int], algo: str = "govm", *, precision: st
     mine = shard_batches(k, world)[rank]
 
     if transport == "auto":
-        transport = "p2p" if on_gpu and backend == "nccl" else "collective"
+        transport = "p2p" if on_gpu else "collective"
     if transport == "p2p":
         # every rank must be able to reach the root's HBM; agree on it
         rdev = [dev.index if on_gpu else -1]
@@ -253,17 +253,22 @@ def apsp_sharded(g, sources: Sequence[int], algo: str = "govm", *, precision: st
             stats_local.append((lo, solve(lo, hi, rows)))
             local[lo] = rows
         plan = shard_batches(k, world)
+        # gloo moves host memory only: stage device rows through the host
+        staged = on_gpu and backend != "nccl"
         if rank == root:
             reqs = []
             for r in range(world):
                 if r == root:
                     continue
                 for lo, hi in plan[r]:
-                    reqs.append(dist.irecv(tile[lo:hi], src=r, group=group))
-            for q in reqs:
+                    buf = torch.empty((hi - lo, n), dtype=out_dtype) if staged else tile[lo:hi]
+                    reqs.append((dist.irecv(buf, src=r, group=group), lo, hi, buf))
+            for q, lo, hi, buf in reqs:
                 q.wait()
+                if staged:
+                    tile[lo:hi].copy_(buf)
         else:
-            reqs = [dist.isend(local[lo], dst=root, group=group) for lo, _ in mine]
+            reqs = [dist.isend(local[lo].cpu() if staged else local[lo], dst=root, group=group) for lo, _ in mine]
             for q in reqs:
                 q.wait()
     if on_gpu:
