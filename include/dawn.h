@@ -162,6 +162,11 @@ int dawn_solver_result(dawn_solver_t s, double* dist_out, int64_t* pred_out,
 int dawn_solver_round_profile(dawn_solver_t s, uint64_t* out, int64_t cap_rounds, int64_t* nrounds,
                               void* stream);
 
+/* Debug (DAWN_F_PROFILE solvers): per-CTA end times (ns, globaltimer) of the
+ * S and X work of the first 64 rounds of the last solve, before each phase's
+ * grid barrier: out[(round * 2 + phase) * grid + cta], grid in *grid_out. */
+int dawn_solver_cta_profile(dawn_solver_t s, uint64_t* out, int64_t cap_rounds, int* grid_out, void* stream);
+
 /* Multi-source: independent solves from sources[0..k) (host int64 array) in
  * the given order — mssp (solver.py:426-457).  Uses the batched kernel
  * (dawn_mssp_batch) when eligible and k >= the "batch_min_sources" tuning

@@ -92,6 +92,7 @@ struct dawn_solver_s {
   double* dbuf = nullptr;
   int64_t* pbuf = nullptr;
   unsigned long long* prof = nullptr;  // per-round timeline (DAWN_F_PROFILE)
+  unsigned long long* cta_prof = nullptr;  // debug per-CTA phase ends (DAWN_F_PROFILE, 256 rounds)
   unsigned prof_cap = 0;
   int grid = 1;       // co-resident CTAs of the plain persistent kernel
   int grid_pred = 1;  // ... of the predecessor-tracking instance
@@ -448,6 +449,7 @@ struct Impl {
     P.dense_edges = (unsigned long long)std::max(1.0, s->dense_edges_per_node * (double)g->n);
     P.prof = s->prof;
     P.prof_cap = s->prof_cap;
+    P.cta_prof = s->cta_prof;
     return P;
   }
 
@@ -690,6 +692,8 @@ struct Impl {
     if (s->flags & DAWN_F_PROFILE) {
       s->prof_cap = 1u << 16;
       CK(cudaMalloc(&s->prof, 32 * (size_t)s->prof_cap));
+      CK(cudaMalloc(&s->cta_prof, 8 * 2 * 2048 * (size_t)CTA_PROF_ROUNDS));
+      CK(cudaMemset(s->cta_prof, 0, 8 * 2 * 2048 * (size_t)CTA_PROF_ROUNDS));
     }
     return setup(s);
   }
@@ -731,6 +735,7 @@ static void solver_free(dawn_solver_t s) {
   cudaFreeHost(s->st_host);
   cudaFree(s->dbuf);
   cudaFree(s->prof);
+  cudaFree(s->cta_prof);
   cudaFree(s->bd);
   for (int i = 0; i < 4; ++i) cudaFree(s->bmask[i]);
   cudaFree(s->bqnode);
@@ -923,6 +928,18 @@ extern "C" int dawn_solver_round_profile(dawn_solver_t s, uint64_t* out, int64_t
   const int64_t k = std::min<int64_t>(done, cap_rounds);
   if (out && k > 0) CK(cudaMemcpy(out, s->prof, 32 * (size_t)k, cudaMemcpyDeviceToHost));
   if (nrounds) *nrounds = done;
+  return DAWN_OK;
+}
+
+extern "C" int dawn_solver_cta_profile(dawn_solver_t s, uint64_t* out, int64_t cap_rounds, int* grid_out,
+                                       void* stream) {
+  if (!s || !s->cta_prof) return fail(DAWN_EINVAL, "solver was created without DAWN_F_PROFILE");
+  cudaStream_t st = (cudaStream_t)stream;
+  CK(cudaSetDevice(s->g->device));
+  CK(cudaStreamSynchronize(st));
+  const int64_t k = std::min<int64_t>(cap_rounds, (int64_t)CTA_PROF_ROUNDS);
+  if (grid_out) *grid_out = s->grid;
+  if (out && k > 0) CK(cudaMemcpy(out, s->cta_prof, 8 * 2 * (size_t)s->grid * (size_t)k, cudaMemcpyDeviceToHost));
   return DAWN_OK;
 }
 

@@ -65,6 +65,7 @@ struct KParams {
   unsigned long long dense_edges;      // a round relaxing >= this many edges builds the next frontier densely
   unsigned long long* prof;            // optional per-round timeline (4 words/round) or nullptr
   unsigned prof_cap;                   // rounds the timeline can hold
+  unsigned long long* cta_prof;        // debug: per-CTA S/X work end times [round][2][grid], or nullptr
 };
 
 constexpr int WPB = NT / 32;       // warps per CTA
@@ -78,6 +79,7 @@ constexpr int WPB = NT / 32;       // warps per CTA
 #define DAWN_XITEMS_WIDE 14
 #endif
 constexpr int XI_NARROW = 8;
+constexpr unsigned CTA_PROF_ROUNDS = 64;  // rounds of the per-CTA debug timeline
 constexpr int XI_WIDE = DAWN_XITEMS_WIDE;
 constexpr int WT_MIN = 32 * (XI_NARROW < XI_WIDE ? XI_NARROW : XI_WIDE);
 
@@ -848,6 +850,8 @@ __global__ void __launch_bounds__(NT, DAWN_MIN_BLOCKS) dawn_persistent(KParams<V
       } else {
         phase_snapshot<V, EI, XI>(P, p);
       }
+      if (P.cta_prof != nullptr && r < CTA_PROF_ROUNDS && threadIdx.x == 0)
+        P.cta_prof[((size_t)r * 2 + 0) * gridDim.x + blockIdx.x] = globaltimer();
       grid_sync(&st->bar);
       // ---- termination (solver.py:284-285, :313-317, :356-358, :388-395) ----
       if (r >= 2) {
@@ -898,6 +902,10 @@ __global__ void __launch_bounds__(NT, DAWN_MIN_BLOCKS) dawn_persistent(KParams<V
     phase_expand<V, EI, false, RAW, XI, FB>(P, p, r, dense, s, acc_w, acc_fd, acc_multi, round_w);
     round_w = __reduce_add_sync(0xffffffffu, round_w);
     if ((threadIdx.x & 31) == 0 && round_w) atomicAdd(&st->wround[p], (unsigned long long)round_w);
+    if (P.cta_prof != nullptr && r < CTA_PROF_ROUNDS) {
+      __syncthreads();
+      if (threadIdx.x == 0) P.cta_prof[((size_t)r * 2 + 1) * gridDim.x + blockIdx.x] = globaltimer();
+    }
     grid_sync(&st->bar);
     if (leader) st->resume_x = 0u;  // every CTA has read it (first barrier passed)
     if constexpr (WITH_PRED) {

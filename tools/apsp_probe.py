@@ -20,6 +20,7 @@ def main():
     ap.add_argument("--k", type=int, default=1024)
     ap.add_argument("--single", type=int, default=32)
     ap.add_argument("--algo", default="govm")
+    ap.add_argument("--order", default="id", help="batch grouping of the sources: id | degree | random")
     a = ap.parse_args()
     import numpy as np
     import torch
@@ -32,6 +33,10 @@ def main():
     degh = deg.cpu().numpy()
     rng = np.random.default_rng(5)
     src = sorted(int(x) for x in rng.choice(np.flatnonzero(degh > 0), size=a.k, replace=False))
+    if a.order == "degree":
+        src = sorted(src, key=lambda x: (-int(degh[x]), x))
+    elif a.order == "random":
+        src = [src[i] for i in np.random.default_rng(9).permutation(len(src))]
     tile = torch.empty((a.k, dg.n), dtype=torch.float32, device="cuda")
     MS.mssp_tile(dg, src[:64], a.algo, out=tile[:64], stats=True)  # warm
     torch.cuda.synchronize()

@@ -81,6 +81,25 @@ def main():
         rate = x["edges"] / (x["x_us"] * 1e3) if x["x_us"] > 0 else 0
         print(f"{x['round']:>4} {x['entries']:>10} {x['edges']:>12} {x['s_us']:>8.1f} {x['x_us']:>9.1f} {rate:>8.1f}")
     print(f"sum S {tot_s:.1f} us, sum X {tot_x:.1f} us")
+    # per-CTA end of S / X work relative to the phase start (imbalance vs throughput)
+    gridc = ctypes.c_int(0)
+    cp = (ctypes.c_uint64 * (2 * 2048 * 64))()
+    N.check(L.dawn_solver_cta_profile(s, cp, 64, ctypes.byref(gridc), stream))
+    G = gridc.value
+    print(f"{'r':>4} {'S min':>7} {'S med':>7} {'S max':>7} {'X min':>7} {'X med':>7} {'X max':>7}  (us after phase start, {G} CTAs)")
+    import statistics as stt
+    for x in rows:
+        r = x["round"]
+        if r >= 64:
+            break
+        t0, t1 = buf[4 * r], buf[4 * r + 1]
+        se = [cp[(r * 2 + 0) * G + b] for b in range(G)]
+        xe = [cp[(r * 2 + 1) * G + b] for b in range(G)]
+        if min(se) == 0 or min(xe) == 0:
+            continue
+        fs = [(v - t0) / 1e3 for v in se]
+        fx = [(v - t1) / 1e3 for v in xe]
+        print(f"{r:>4} {min(fs):>7.1f} {stt.median(fs):>7.1f} {max(fs):>7.1f} {min(fx):>7.1f} {stt.median(fx):>7.1f} {max(fx):>7.1f}")
     if a.out:
         Path(a.out).write_text(json.dumps({"solve_ms": times, "rounds": rows, "R": st.relaxations,
                                            "W": st.writes, "steps": st.outer_steps}, indent=1))
