@@ -114,6 +114,9 @@ int dawn_solver_destroy(dawn_solver_t s);
  *   value*n edges records its writes as plain stamps and the next frontier is
  *   rebuilt by a coalesced sweep; lighter rounds enqueue written nodes.
  *   "batch_min_sources" (default 4): dawn_mssp batches k >= value sources.
+ *   "batch_sparse_util" (default 4): batched rounds whose rows carry fewer
+ *   active sources per edge than this relax lane by lane (0 = never, 33 =
+ *   always).
  *   "wide_tiles" (default -1 = auto): 1 / 0 forces wide (14 edges per lane)
  *   or narrow (8) X-phase warp tiles for 4-byte values; auto = wide when
  *   m >= 2^25 and m >= 8n.

@@ -102,7 +102,8 @@ struct dawn_solver_s {
   bool wide = false;
   int fb_pref = -1;                   // tunable "bitmap_frontier": -1 auto, 0 off, 1 on
   bool fb = false;
-  double batch_min_sources = 4;       // tunable: dawn_mssp batches when k >= this  // tunable: dense frontier build after rounds relaxing >= this * n edges
+  double batch_min_sources = 4;       // tunable: dawn_mssp batches when k >= this
+  double batch_sparse_util = 4;       // tunable: batched rounds averaging < this active sources per edge go lane-sparse  // tunable: dense frontier build after rounds relaxing >= this * n edges
   int ebits = 32;
   int logn = 0;
   // batched multi-source workspace (allocated on first use, kept)
@@ -617,6 +618,7 @@ struct Impl {
     for (int l = 0; l < BL; ++l) P.src[l] = l < nl ? (uint32_t)src[l] : 0xFFFFFFFFu;
     P.ebits = s->ebits;
     P.algo = algo;
+    P.sparse_util = (uint32_t)s->batch_sparse_util;
     P.prof = s->prof;
     P.prof_cap = s->prof_cap;
     return P;
@@ -788,6 +790,11 @@ extern "C" int dawn_solver_tune(dawn_solver_t s, const char* key, double value) 
     s->fb_pref = (int)value;
     CK(cudaSetDevice(s->g->device));
     return DISPATCH(s->g, setup(s));
+  }
+  if (!strcmp(key, "batch_sparse_util")) {
+    if (!(value >= 0.0 && value <= 33.0)) return fail(DAWN_EINVAL, "batch_sparse_util must be in [0, 33]");
+    s->batch_sparse_util = value;
+    return DAWN_OK;
   }
   if (!strcmp(key, "batch_min_sources")) {
     if (!(value >= 0.0)) return fail(DAWN_EINVAL, "batch_min_sources must be >= 0");

@@ -44,6 +44,7 @@ constexpr int BWT = 32;   // virtual edges per warp tile (<= 32 rows per tile)
 
 struct BState {
   unsigned long long res[2];   // packed frontier reservation (count << ebits | edges), by round parity
+  unsigned long long le[2];    // lane-edges (relaxations) of the round with this parity
   unsigned bar;                // grid barrier word (never reset)
   unsigned wrote[2];           // lanes that lowered any node in the round with this parity
   unsigned guard;              // lanes whose source guard fired (solver.py:299-303)
@@ -76,6 +77,7 @@ struct BParams {
   uint32_t src[BL];                // lane -> source node (0xFFFFFFFF = unused lane)
   int ebits;
   int algo;                        // 0 = GOVM, 1 = GSVM
+  uint32_t sparse_util;            // a round with lane-edges < this * edges relaxes lane-sparse
   unsigned long long* prof;        // optional per-round timeline, 4 words/round, or nullptr
   unsigned prof_cap;
 };
@@ -84,6 +86,8 @@ template <class V, class EI>
 struct __align__(16) BSmem {
   unsigned long long scr64[NT / 32];
   unsigned long long basepk;
+  unsigned rl[BL];            // relaxations per source lane counted by lane-sparse rounds (< 2^32 per CTA)
+  uint32_t src[BL];           // lane -> source node (lane-sparse source guard)
 };
 
 template <class V> struct BEdge;
@@ -259,13 +263,16 @@ __device__ void bphase_build(const BParams<V, EI>& P, uint32_t r, uint32_t activ
     if (threadIdx.x == 0 && tot != 0ull) s.basepk = atomicAdd(&P.st->res[r & 1], tot);
     __syncthreads();
     if (!__any_sync(0xffffffffu, sel != 0u)) continue;
-    if (P.prof != nullptr && r < P.prof_cap) {  // lane-edges of round r (profile only)
+    {  // lane-edges of round r: chooses the relax mode of the X phase (and the profile)
       unsigned long long le = 0;
 #pragma unroll
       for (int j = 0; j < ITEMS; ++j)
         if ((sel >> j) & 1u) le += (unsigned long long)__popc(F[j]) * (unsigned long long)(rp[j + 1] - rp[j]);
       le = warp_sum_u64(le);
-      if (lane == 0 && le) atomicAdd(P.prof + 4 * r + 3, le);
+      if (lane == 0 && le) {
+        atomicAdd(&P.st->le[r & 1], le);
+        if (P.prof != nullptr && r < P.prof_cap) atomicAdd(P.prof + 4 * r + 3, le);
+      }
     }
     if (!sel) continue;
     // this thread's entries: metadata, tile marks and the 32-lane snapshot
@@ -390,9 +397,14 @@ __device__ __forceinline__ void btile_issue(const BParams<V, EI>& P, EI t, EI E,
   if (lane < X.len) BEdge<V>::load(P, base + e0 + (EI)lane, X.col, X.w);
 }
 
-template <class V, class EI>
+// SPARSE: lane-sparse rounds (few active sources per frontier row, e.g. the
+// first rounds, where every source still explores its own neighbourhood): a
+// thread owns one edge and walks the row's set lanes one by one (scalar
+// gathers), instead of 8 threads covering all 32 lanes of the distance line.
+template <class V, class EI, bool SPARSE>
 __device__ void bphase_expand(const BParams<V, EI>& P, uint32_t r, const uint32_t (&msrc)[BLanes<V>::LPT],
-                              unsigned& guard, unsigned& wrote, unsigned long long (&accR)[BLanes<V>::LPT]) {
+                              unsigned& guard, unsigned& wrote, unsigned long long (&accR)[BLanes<V>::LPT],
+                              BSmem<V, EI>& sm) {
   using CD = Codec<V, true>;
   using K = typename CD::K;
   using WB = typename CD::WB;
@@ -443,6 +455,28 @@ __device__ void bphase_expand(const BParams<V, EI>& P, uint32_t r, const uint32_
   constexpr uint32_t FMASK = LPT == 4 ? 0x01010101u : 0x00010001u;
   constexpr int FBITS = LPT == 4 ? 8 : 16;
   for (;;) {
+    if constexpr (SPARSE) {
+      // ---- relax tile A, lane-sparse: lane j = edge j, loop over the row's lanes ----
+      const uint32_t mrow = __shfl_sync(0xffffffffu, A.rmask, A.kr & 31);
+      uint32_t lanes = lane < A.len ? mrow : 0u;
+      const size_t rowk = (size_t)(A.i0 + A.kr) * BL;
+      while (lanes) {
+        const uint32_t l = __ffs(lanes) - 1;
+        lanes &= lanes - 1u;
+        atomicAdd(&sm.rl[l], 1u);  // relaxation of source lane l (solver.py:297, :372)
+        const K c = CD::relax(CD::dec(__ldca(P.qkey + rowk + l)), A.w);
+        const K cur = __ldca(P.bd + (size_t)A.col * BL + l);
+        if (c < CAP && c < cur) {
+          if (A.col == sm.src[l]) {
+            guard |= 1u << l;  // source guard (solver.py:299-303)
+          } else {
+            atomicMin(P.bd + (size_t)A.col * BL + l, c);
+            atomicOr(P.nmask + A.col, 1u << l);
+            wrote |= 1u << l;
+          }
+        }
+      }
+    } else {
     // ---- relax tile A ----
     uint32_t ck = 0xFFFFFFFFu;  // this thread's current row (relative to A.i0)
     K cs[LPT];
@@ -500,6 +534,7 @@ __device__ void bphase_expand(const BParams<V, EI>& P, uint32_t r, const uint32_
     }
 #pragma unroll
     for (int i = 0; i < LPT; ++i) accR[i] += (rcp >> (FBITS * i)) & ((1u << FBITS) - 1u);
+    }  // dense lanes
     // ---- advance the pipeline ----
     if (Bt.len == 0) break;  // warp-uniform: no next tile
     t += GW;
@@ -535,6 +570,11 @@ __global__ void __launch_bounds__(NT, DAWN_BATCH_MIN_BLOCKS) dawn_batch_persiste
   uint32_t lastw = 0;  // this lane's last writing round (identical in every thread of the lane)
   const uint32_t valid = __ballot_sync(0xffffffffu, lane < P.nlanes);
   uint32_t active = valid;
+  if (threadIdx.x < BL) {
+    s.rl[threadIdx.x] = 0u;
+    s.src[threadIdx.x] = P.src[threadIdx.x];
+  }
+  __syncthreads();
   uint32_t r = 1;
   // Round r = B(r) [builds into res[r&1]] | barrier | X(r) [ORs its writers into
   // wrote[r&1]] | barrier.  Double-buffered by parity, so every reset happens
@@ -551,7 +591,10 @@ __global__ void __launch_bounds__(NT, DAWN_BATCH_MIN_BLOCKS) dawn_batch_persiste
     // ---- B phase ----
     const bool prof = leader && P.prof != nullptr && r < P.prof_cap;
     if (prof) P.prof[4 * r + 0] = globaltimer();
-    if (leader) st->res[(r + 1) & 1] = 0ull;  // last read by X(r-1), next written by B(r+1)
+    if (leader) {  // last read by X(r-1), next written by B(r+1)
+      st->res[(r + 1) & 1] = 0ull;
+      st->le[(r + 1) & 1] = 0ull;
+    }
     bphase_build<V, EI>(P, r, active, s, accW, accFD, accMW);
     grid_sync(&st->bar);
     // ---- X phase ----
@@ -561,7 +604,13 @@ __global__ void __launch_bounds__(NT, DAWN_BATCH_MIN_BLOCKS) dawn_batch_persiste
     }
     if (leader) st->wrote[(r + 1) & 1] = 0u;  // last read at the top of round r, next written by X(r+1)
     unsigned wrote = 0;
-    bphase_expand<V, EI>(P, r, msrc, guard, wrote, accR);
+    {
+      // lane-sparse relax when the round's rows carry few active sources on average
+      const unsigned long long E = pk_edges(ldcg(&st->res[r & 1]), P.ebits);
+      const unsigned long long LE = ldcg(&st->le[r & 1]);
+      if (LE < (unsigned long long)P.sparse_util * E) bphase_expand<V, EI, true>(P, r, msrc, guard, wrote, accR, s);
+      else bphase_expand<V, EI, false>(P, r, msrc, guard, wrote, accR, s);
+    }
     wrote = __reduce_or_sync(0xffffffffu, wrote);
     if (lane == 0 && wrote) atomicOr(&st->wrote[r & 1], wrote);
     grid_sync(&st->bar);
@@ -597,6 +646,7 @@ __global__ void __launch_bounds__(NT, DAWN_BATCH_MIN_BLOCKS) dawn_batch_persiste
     unsigned long long sum = 0;
 #pragma unroll
     for (int w = 0; w < NT / 32; ++w) sum += red[w][l][f];
+    if (f == 0) sum += (unsigned long long)s.rl[l];  // relaxations counted by lane-sparse rounds
     if (sum) {
       unsigned long long* dst = f == 0 ? st->R : f == 1 ? st->W : f == 2 ? st->FD : st->MW;
       atomicAdd(dst + l, sum);
@@ -619,6 +669,7 @@ __global__ void dawn_batch_init(BParams<V, EI> P) {
   if (l == 0) {
     BState* st = P.st;
     st->res[0] = st->res[1] = 0ull;
+    st->le[0] = st->le[1] = 0ull;
     st->wrote[0] = st->wrote[1] = 0u;
     st->guard = 0u;
     st->rounds = 0u;

@@ -35,8 +35,16 @@ def check_rows(g, sources, algo, tile, stats, precision=None):
         assert stats[i].as_dict() == st.as_dict(), (algo, i, s)
 
 
+@pytest.fixture(params=[4, 0, 33], ids=["auto", "dense-lanes", "sparse-lanes"])
+def lane_mode(request):
+    """Batched relax: default lane-sparse policy, never, always."""
+    P.set_tuning(batch_sparse_util=request.param)
+    yield request.param
+    P.set_tuning(batch_sparse_util=4)
+
+
 @pytest.mark.parametrize("seed", range(10))
-def test_batch_random_vs_single(gpu, seed):
+def test_batch_random_vs_single(gpu, seed, lane_mode):
     rng = np.random.default_rng(100 + seed)
     n = int(rng.integers(2, 600))
     m = int(rng.integers(0, 8 * n))
@@ -60,7 +68,7 @@ def test_batch_is_the_mssp_path(gpu):
         assert same(dv.dist, dv1.dist) and st.as_dict() == st1.as_dict()
 
 
-def test_batch_rmat14_int_vs_reference_port(gpu):
+def test_batch_rmat14_int_vs_reference_port(gpu, lane_mode):
     g = G.rmat_graph(14, 8, weights="int")  # config 1's shape
     rng = np.random.default_rng(5)
     deg = np.diff(g.row_ptr)
@@ -76,7 +84,7 @@ def test_batch_rmat14_int_vs_reference_port(gpu):
     check_rows(g, src[12:20], "govm", t[12:20], stats[12:20])
 
 
-def test_batch_fp32_tile(gpu):
+def test_batch_fp32_tile(gpu, lane_mode):
     g = G.rmat_graph(15, 16, weights="f32")
     src = list(range(0, 2000, 31))
     tile, stats = MS.mssp_tile(g, src, "govm", precision="fp32", out_dtype=torch.float32)

@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--single", type=int, default=32)
     ap.add_argument("--algo", default="govm")
     ap.add_argument("--order", default="id", help="batch grouping of the sources: id | degree | random")
+    ap.add_argument("--util", type=float, default=None, help="batch_sparse_util tuning knob")
     a = ap.parse_args()
     import numpy as np
     import torch
@@ -37,6 +38,9 @@ def main():
         src = sorted(src, key=lambda x: (-int(degh[x]), x))
     elif a.order == "random":
         src = [src[i] for i in np.random.default_rng(9).permutation(len(src))]
+    if a.util is not None:
+        for fl in (0, N.F_PROFILE):
+            N.check(N.lib().dawn_solver_tune(dg.solver(fl), b"batch_sparse_util", a.util))
     tile = torch.empty((a.k, dg.n), dtype=torch.float32, device="cuda")
     MS.mssp_tile(dg, src[:64], a.algo, out=tile[:64], stats=True)  # warm
     torch.cuda.synchronize()
