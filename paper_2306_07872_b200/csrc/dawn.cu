@@ -97,13 +97,13 @@ struct dawn_solver_s {
   int grid = 1;       // co-resident CTAs of the plain persistent kernel
   int grid_pred = 1;  // ... of the predecessor-tracking instance
   size_t smem = 0;
-  double dense_edges_per_node = 0.5;
+  double dense_edges_per_node = 0.5;  // tunable: dense frontier build after rounds relaxing >= this * n edges
   int wide_pref = -1;                 // tunable "wide_tiles": -1 auto, 0 narrow, 1 wide X-phase tiles
   bool wide = false;
   int fb_pref = -1;                   // tunable "bitmap_frontier": -1 auto, 0 off, 1 on
   bool fb = false;
   double batch_min_sources = 4;       // tunable: dawn_mssp batches when k >= this
-  double batch_sparse_util = 4;       // tunable: batched rounds averaging < this active sources per edge go lane-sparse  // tunable: dense frontier build after rounds relaxing >= this * n edges
+  double batch_sparse_util = 4;       // tunable: batched rounds averaging < this active sources per edge go lane-sparse
   int ebits = 32;
   int logn = 0;
   // batched multi-source workspace (allocated on first use, kept)
