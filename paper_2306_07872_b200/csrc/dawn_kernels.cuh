@@ -218,57 +218,55 @@ __device__ void phase_compact(const KParams<V, EI>& P, int p, uint32_t r, Smem<V
   const uint32_t nchunks = (n + TILE - 1) / TILE;
   const bool gsvm = P.algo == 1;
   const int eb = P.ebits;
-  // stamps of the thread's next chunk are prefetched one iteration ahead
-  uint32_t nst[ITEMS];
-  auto load_stamps = [&](uint32_t c, uint32_t (&o)[ITEMS]) {
-    const uint32_t u = c * TILE + threadIdx.x * ITEMS;
-    if (u + ITEMS <= n) {
-      ldcg8<uint32_t>(P.stamp + u, o);
-    } else {
-#pragma unroll
-      for (int j = 0; j < ITEMS; ++j) o[j] = (u + j < n) ? ldcg(P.stamp + u + j) : 0u;
-    }
-  };
-  if (blockIdx.x < nchunks) load_stamps(blockIdx.x, nst);
-  for (uint32_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
-    const uint32_t u0 = c * TILE + threadIdx.x * ITEMS;
-    uint32_t stv[ITEMS];
-#pragma unroll
-    for (int j = 0; j < ITEMS; ++j) stv[j] = nst[j];
-    if (c + gridDim.x < nchunks) load_stamps(c + gridDim.x, nst);
+  // Everything a chunk needs — stamps, write states, keys, row bounds — is
+  // loaded one iteration ahead, unconditionally: a CTA walks ~7 chunks per
+  // phase and a per-chunk chain of dependent loads (stamps -> keys/rows/state)
+  // cost ~1.5 us each (timeline in profiles/r01_experiments.md).  The extra
+  // bytes (keys and row bounds of chunks without writes) are L2 reads of
+  // arrays the round touches anyway.
+  struct Pre {
+    uint32_t st[ITEMS];
     K keys[ITEMS];
     EI rp[ITEMS + 1];
+    uint2 ws;
+  };
+  auto load_chunk = [&](uint32_t c, Pre& o) {
+    const uint32_t u = c * TILE + threadIdx.x * ITEMS;
+    if (u + ITEMS <= n) {
+      ldcg8<uint32_t>(P.stamp + u, o.st);
+      ldcg8<K>(P.dist + u, o.keys);
+      ldg8<EI>(P.row_ptr + u, *reinterpret_cast<EI(*)[ITEMS]>(o.rp));
+      o.rp[ITEMS] = __ldg(P.row_ptr + u + ITEMS);
+      o.ws = __ldcg(reinterpret_cast<const uint2*>(P.wstate + u));
+    } else {
+      uint8_t* b = reinterpret_cast<uint8_t*>(&o.ws);
+#pragma unroll
+      for (int j = 0; j < ITEMS; ++j) {
+        o.st[j] = (u + j < n) ? ldcg(P.stamp + u + j) : 0u;
+        o.keys[j] = (u + j < n) ? ldcg(P.dist + u + j) : VT::INF;
+        o.rp[j] = (u + j <= n) ? __ldg(P.row_ptr + u + j) : (EI)0;
+        b[j] = (u + j < n) ? ldcg(P.wstate + u + j) : (uint8_t)0;
+      }
+      o.rp[ITEMS] = (u + ITEMS <= n) ? __ldg(P.row_ptr + u + ITEMS) : (EI)0;
+    }
+  };
+  Pre nx;
+  if (blockIdx.x < nchunks) load_chunk(blockIdx.x, nx);
+  for (uint32_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+    const uint32_t u0 = c * TILE + threadIdx.x * ITEMS;
+    const Pre cur = nx;
+    if (c + gridDim.x < nchunks) load_chunk(c + gridDim.x, nx);
+    const K (&keys)[ITEMS] = cur.keys;
+    const EI (&rp)[ITEMS + 1] = cur.rp;
     const bool full = u0 + ITEMS <= n;
     unsigned wm = 0;  // lowered in round r-1
 #pragma unroll
-    for (int j = 0; j < ITEMS; ++j) wm |= (unsigned)(stv[j] == r - 1 && u0 + j < n) << j;
+    for (int j = 0; j < ITEMS; ++j) wm |= (unsigned)(cur.st[j] == r - 1 && u0 + j < n) << j;
     const unsigned want = gsvm ? ((u0 < n) ? 0xFFu : 0u) : wm;
-    // keys, row bounds and write states: one batch of vector loads
     unsigned sel = 0;
     uint32_t mycnt = 0;
     EI mydeg = 0;
-    uint2 ws = make_uint2(0, 0);
-    if (wm) {
-      if (full) ws = __ldcg(reinterpret_cast<const uint2*>(P.wstate + u0));
-      else {
-        uint8_t* b = reinterpret_cast<uint8_t*>(&ws);
-#pragma unroll
-        for (int j = 0; j < ITEMS; ++j) b[j] = (u0 + j < n) ? ldcg(P.wstate + u0 + j) : (uint8_t)0;
-      }
-    }
     if (want) {
-      if (full) {
-        ldcg8<K>(P.dist + u0, keys);
-        ldg8<EI>(P.row_ptr + u0, *reinterpret_cast<EI(*)[ITEMS]>(rp));
-        rp[ITEMS] = __ldg(P.row_ptr + u0 + ITEMS);
-      } else {
-#pragma unroll
-        for (int j = 0; j < ITEMS; ++j) {
-          keys[j] = (u0 + j < n) ? ldcg(P.dist + u0 + j) : VT::INF;
-          rp[j] = (u0 + j <= n) ? __ldg(P.row_ptr + u0 + j) : (EI)0;
-        }
-        rp[ITEMS] = (u0 + ITEMS <= n) ? __ldg(P.row_ptr + u0 + ITEMS) : (EI)0;
-      }
 #pragma unroll
       for (int j = 0; j < ITEMS; ++j) {
         if (((want >> j) & 1u) && u0 + j < n && keys[j] != VT::INF && rp[j + 1] > rp[j]) {
@@ -280,6 +278,7 @@ __device__ void phase_compact(const KParams<V, EI>& P, int p, uint32_t r, Smem<V
     }
     // write bookkeeping for round r-1 (first_discoveries, >= 2-round nodes)
     if (wm) {
+      uint2 ws = cur.ws;
       uint8_t* b = reinterpret_cast<uint8_t*>(&ws);
 #pragma unroll
       for (int j = 0; j < ITEMS; ++j) {
@@ -297,7 +296,7 @@ __device__ void phase_compact(const KParams<V, EI>& P, int p, uint32_t r, Smem<V
           if (u0 + j < n) P.wstate[u0 + j] = b[j];
       }
     }
-    // 4. place the chunk's entries: one packed scan, one reservation
+    // place the chunk's entries: one packed scan, one reservation
     const unsigned long long mine = ((unsigned long long)mycnt << eb) | (unsigned long long)mydeg;
     unsigned long long tot;
     const unsigned long long incl = block_incl_sum<unsigned long long>(mine, s.scr64, &tot);
