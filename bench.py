@@ -420,9 +420,9 @@ def ours(args):
     if host is not None:
         import ctypes as C
 
-        rp_h = torch.from_numpy(np.ascontiguousarray(host.row_ptr)).pin_memory()
-        col_h = torch.from_numpy(np.ascontiguousarray(host.col)).pin_memory()
-        val_h = torch.from_numpy(np.ascontiguousarray(host.val)).pin_memory()
+        rp_h = torch.from_numpy(np.array(host.row_ptr)).pin_memory()
+        col_h = torch.from_numpy(np.array(host.col)).pin_memory()
+        val_h = torch.from_numpy(np.array(host.val)).pin_memory()
         out_h = torch.empty(n, dtype=torch.float64).pin_memory()
         m_edges = int(host.m)
         st_e = N.Stats()
