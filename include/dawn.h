@@ -62,6 +62,12 @@ extern "C" {
 #define DAWN_F_NEGCHECK 2u    /* early negative-cycle exit via predecessor-graph cycle check
                                  (integer types only; same verdict as the n-round cap, solver.py:394-395) */
 #define DAWN_F_PROFILE 4u     /* solver flag: record a per-round device timeline (globaltimer) */
+#define DAWN_F_ASYNC 8u       /* solve flag: "async" schedule — a frontier row is relaxed with its LIVE
+                                 distance (possibly lowered earlier in the same round, as in the
+                                 reference's in-place order, solver.py:369-385) instead of the
+                                 round-start snapshot.  Same distances and negative-cycle flag (the
+                                 same greatest fixpoint); work counters become timing-dependent.
+                                 Ignored with DAWN_F_PRED / the negative-cycle check. */
 
 typedef struct dawn_graph_s* dawn_graph_t;
 typedef struct dawn_solver_s* dawn_solver_t;

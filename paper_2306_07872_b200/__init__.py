@@ -6,7 +6,16 @@ hand-written sm_100a CUDA kernels behind the C ABI in ``include/dawn.h``
 (``libdawn.so``, loaded through ctypes).  There is no CPU fallback.
 """
 
-from .device import DeviceGraph, clear_cache, device_graph, get_default_precision, set_default_precision, set_tuning
+from .device import (
+    DeviceGraph,
+    clear_cache,
+    device_graph,
+    get_default_precision,
+    get_default_schedule,
+    set_default_precision,
+    set_default_schedule,
+    set_tuning,
+)
 from .graph import (
     CsrGraph,
     EdgeList,
@@ -65,6 +74,8 @@ __all__ = [
     "set_default_precision",
     "get_default_precision",
     "set_tuning",
+    "set_default_schedule",
+    "get_default_schedule",
     "MuReport",
     "run_mu_experiment",
 ]

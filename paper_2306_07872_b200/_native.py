@@ -33,6 +33,7 @@ GOVM, GSVM = 0, 1
 F_PRED = 1
 F_NEGCHECK = 2
 F_PROFILE = 4
+F_ASYNC = 8
 
 # every symbol include/dawn.h declares (checked by tests/test_abi.py)
 EXPORTS = (

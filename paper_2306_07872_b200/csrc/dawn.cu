@@ -451,6 +451,7 @@ struct Impl {
     P.prof = s->prof;
     P.prof_cap = s->prof_cap;
     P.cta_prof = s->cta_prof;
+    P.live = (s->run_flags & DAWN_F_ASYNC) && !P.pred_on ? 1 : 0;
     return P;
   }
 
@@ -824,7 +825,7 @@ static int do_begin(dawn_solver_t s, int64_t source, int algo, unsigned flags, c
   s->source = source;
   s->algo = algo;
   s->last_batch = false;
-  s->run_flags = flags & (s->flags | DAWN_F_NEGCHECK);
+  s->run_flags = flags & (s->flags | DAWN_F_NEGCHECK | DAWN_F_ASYNC);
   if ((s->run_flags & DAWN_F_NEGCHECK) && !s->pred) s->run_flags &= ~DAWN_F_NEGCHECK;
   s->active = true;
   return DISPATCH(s->g, begin(s, st));

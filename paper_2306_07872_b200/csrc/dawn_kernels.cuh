@@ -66,6 +66,7 @@ struct KParams {
   unsigned long long* prof;            // optional per-round timeline (4 words/round) or nullptr
   unsigned prof_cap;                   // rounds the timeline can hold
   unsigned long long* cta_prof;        // debug: per-CTA S/X work end times [round][2][grid], or nullptr
+  int live;                            // async schedule: frontier rows relaxed with their live value (no snapshot)
 };
 
 constexpr int WPB = NT / 32;       // warps per CTA
@@ -545,7 +546,7 @@ __device__ void phase_expand(const KParams<V, EI>& P, int p, uint32_t r, bool de
   if (lane <= il - i0) {
     pf_base = ldcg(qbase + i0 + lane);
     pf_off = ldcg(qoff + i0 + lane);
-    pf_key = ldcg(qkey + i0 + lane);
+    pf_key = (!PRED && P.live) ? ldcg(P.dist + ldcg(qnode + i0 + lane)) : ldcg(qkey + i0 + lane);
     if (PRED) pf_node = ldcg(qnode + i0 + lane);
   }
 
@@ -582,7 +583,7 @@ __device__ void phase_expand(const KParams<V, EI>& P, int p, uint32_t r, bool de
         if (lane <= il - i0) {
           pf_base = ldcg(qbase + i0 + lane);
           pf_off = ldcg(qoff + i0 + lane);
-          pf_key = ldcg(qkey + i0 + lane);
+          pf_key = (!PRED && P.live) ? ldcg(P.dist + ldcg(qnode + i0 + lane)) : ldcg(qkey + i0 + lane);
           if (PRED) pf_node = ldcg(qnode + i0 + lane);
         }
         tr = (lane < 2 && tn + GW < T) ? row_bound(tn + GW, lane) : 0u;
@@ -635,7 +636,7 @@ __device__ void phase_expand(const KParams<V, EI>& P, int p, uint32_t r, bool de
         const uint32_t k = w.mark[j * 32 + lane];
         rowk[j] = k;
         pos[j] = __ldca(qbase + ci0 + k) + e0 + (EI)(j * 32 + lane);
-        rv[j] = CD::dec(__ldca(qkey + ci0 + k));
+        rv[j] = CD::dec((!PRED && P.live) ? ldcg(P.dist + __ldca(qnode + ci0 + k)) : __ldca(qkey + ci0 + k));
       }
     }
     // ---- phase 1b: all edge loads back to back (nothing consumes them yet) ----

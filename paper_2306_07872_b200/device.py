@@ -23,7 +23,9 @@ _cache: "weakref.WeakKeyDictionary[object, dict]" = weakref.WeakKeyDictionary()
 _strong_cache: dict[int, tuple[object, dict]] = {}
 
 _default_precision = "auto"
+_default_schedule = "jacobi"
 _tuning: dict[str, float] = {}
+SCHEDULES = ("jacobi", "async")
 
 
 def set_tuning(**knobs: float) -> None:
@@ -55,6 +57,27 @@ def set_default_precision(precision: str) -> None:
 
 def get_default_precision() -> str:
     return _default_precision
+
+
+def set_default_schedule(schedule: str) -> None:
+    """Process-wide round schedule of the single-source solvers.
+
+    ``jacobi`` (default): every frontier row is relaxed with its value at the
+    start of the round — distances AND work counters are deterministic and
+    equal to the snapshot-Jacobi oracle.  ``async``: rows are relaxed with
+    their live value, which another row may already have lowered in the same
+    round (the reference's in-place order, solver.py:369-385, does the same
+    sequentially): identical distances and negative-cycle flags, fewer
+    relaxations (C2: 212 M instead of 299 M), counters timing-dependent.
+    """
+    global _default_schedule
+    if schedule not in SCHEDULES:
+        raise ValueError(f"unknown schedule {schedule!r}; expected one of {list(SCHEDULES)}")
+    _default_schedule = schedule
+
+
+def get_default_schedule() -> str:
+    return _default_schedule
 
 
 def _current_stream(device: int) -> int:

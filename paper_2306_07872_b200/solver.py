@@ -39,6 +39,7 @@ from typing import Callable, Iterable, Sequence
 import numpy as np
 
 from . import _native as N
+from . import device as _dev
 from .device import DeviceGraph, device_graph
 
 __all__ = [
@@ -233,10 +234,17 @@ def _neg_flags(dg: DeviceGraph) -> int:
 # ---------------------------------------------------------------------------
 # single-source solves
 # ---------------------------------------------------------------------------
-def _solve(g, source: int, algo: int, record_pred: bool, precision: str | None):
+def _schedule_flag(schedule: str | None) -> int:
+    sch = schedule or _dev.get_default_schedule()
+    if sch not in _dev.SCHEDULES:
+        raise ValueError(f"unknown schedule {sch!r}; expected one of {list(_dev.SCHEDULES)}")
+    return N.F_ASYNC if sch == "async" else 0
+
+
+def _solve(g, source: int, algo: int, record_pred: bool, precision: str | None, schedule: str | None = None):
     _check_source(g, int(source))
     dg = device_graph(g, precision=precision)
-    flags = (N.F_PRED if record_pred else 0) | _neg_flags(dg)
+    flags = (N.F_PRED if record_pred else 0) | _neg_flags(dg) | _schedule_flag(schedule)
     with dg.lock:
         s = dg.solver(flags)
         dist = np.empty(dg.n, dtype=np.float64)
@@ -251,7 +259,8 @@ def _solve(g, source: int, algo: int, record_pred: bool, precision: str | None):
     return dv, pv, _stats_from_native(st)
 
 
-def _solve_traced(g, source: int, algo: int, record_pred: bool, trace, precision: str | None):
+def _solve_traced(g, source: int, algo: int, record_pred: bool, trace, precision: str | None,
+                  schedule: str | None = None):
     """Host-synchronised stepping for the ``trace`` hook (solver.py:328-336, :386-387).
 
     ``scanned`` for round r is the set lowered in round r-1 and ``written`` the
@@ -260,7 +269,7 @@ def _solve_traced(g, source: int, algo: int, record_pred: bool, trace, precision
     """
     _check_source(g, int(source))
     dg = device_graph(g, precision=precision)
-    flags = (N.F_PRED if record_pred else 0) | _neg_flags(dg)
+    flags = (N.F_PRED if record_pred else 0) | _neg_flags(dg) | _schedule_flag(schedule)
     L = N.lib()
     with dg.lock:
         s = dg.solver(flags)
@@ -295,26 +304,29 @@ def _solve_traced(g, source: int, algo: int, record_pred: bool, trace, precision
     return dv, pv, _stats_from_native(st)
 
 
-def gsvm_sssp(g, source: int, record_pred: bool = False, *, precision: str | None = None):
+def gsvm_sssp(g, source: int, record_pred: bool = False, *, precision: str | None = None,
+              schedule: str | None = None):
     """Full-rescan SSSP (Alg. 1; reference solver.py:265-321) on the GPU.
 
     Returns ``(DistanceVector, PredecessorVector | None, SolveStats)``.
-    ``precision`` (extension): ``auto``/``fp32``/``fp64``, default from
-    :func:`set_default_precision`.
+    Extensions: ``precision`` — ``auto``/``fp32``/``fp64``, default from
+    :func:`set_default_precision`; ``schedule`` — ``jacobi``/``async``,
+    default from :func:`set_default_schedule`.
     """
-    return _solve(g, source, N.GSVM, record_pred, precision)
+    return _solve(g, source, N.GSVM, record_pred, precision, schedule)
 
 
 def govm_sssp(g, source: int, record_pred: bool = False, trace: Callable | None = None, *,
-              precision: str | None = None):
+              precision: str | None = None, schedule: str | None = None):
     """Frontier SSSP (Alg. 2; reference solver.py:324-399) on the GPU.
 
     ``trace(step, scanned_nodes, written_nodes, distance_snapshot)`` is called
-    after every round from step 2 on, as in the reference.
+    after every round from step 2 on, as in the reference.  ``precision`` and
+    ``schedule`` as in :func:`gsvm_sssp`.
     """
     if trace is not None:
-        return _solve_traced(g, source, N.GOVM, record_pred, trace, precision)
-    return _solve(g, source, N.GOVM, record_pred, precision)
+        return _solve_traced(g, source, N.GOVM, record_pred, trace, precision, schedule)
+    return _solve(g, source, N.GOVM, record_pred, precision, schedule)
 
 
 def seed_source(g, source: int, alpha: list, delta: list, stats: SolveStats | None = None,

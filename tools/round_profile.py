@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--grid", type=int, default=0, help="grid side (>0: 2D grid instead of RMAT)")
     ap.add_argument("--dense", type=float, default=None, help="dense_edges_per_node tuning knob")
     ap.add_argument("--bitmap", type=float, default=None, help="bitmap_edges_per_node tuning knob")
+    ap.add_argument("--tune", action="append", default=[], help="key=value solver tuning (repeatable)")
     a = ap.parse_args()
     import torch
 
@@ -46,6 +47,9 @@ def main():
     s = dg.solver(N.F_PROFILE)
     if a.dense is not None:
         N.check(L.dawn_solver_tune(s, b"dense_edges_per_node", a.dense))
+    for kv in a.tune:
+        k_, v_ = kv.split("=")
+        N.check(L.dawn_solver_tune(s, k_.encode(), float(v_)))
     if a.bitmap is not None:
         N.check(L.dawn_solver_tune(s, b"bitmap_edges_per_node", a.bitmap))
     stream = torch.cuda.current_stream().cuda_stream
