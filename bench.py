@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=120.0, help="seconds for the reference arm's timed steps")
     ap.add_argument("--no-apsp", action="store_true", help="skip the config-3 multi-source leg")
+    ap.add_argument("--schedule", choices=["async", "jacobi"], default="async",
+                    help="round schedule of the headline solve (the other one is timed beside it)")
     ap.add_argument("--apsp-sources", type=int, default=8192)
     ap.add_argument("--apsp-scale", type=int, default=20)
     ap.add_argument("--dist-backend", default="nccl", help="process-group backend (gloo only for the 1-GPU "
@@ -346,11 +348,13 @@ def ours(args):
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
            torch.cuda.Event(enable_timing=True)) for _ in range(K)]
 
-    def step(e=None):
+    sflag = N.F_ASYNC if args.schedule == "async" else 0
+
+    def step(e=None, flags=None):
         flush.zero_()  # evict L2 outside the timed events
         if e is not None:
             e[0].record()
-        N.check(L.dawn_sssp_begin(s, src, N.GOVM, 0, stream))
+        N.check(L.dawn_sssp_begin(s, src, N.GOVM, sflag if flags is None else flags, stream))
         if e is not None:
             e[1].record()
         N.check(L.dawn_sssp_run(s, 0, stream))
@@ -397,8 +401,32 @@ def ours(args):
     t_step = tot_ms / K / 1e3
     value = world * m_reach / t_step / 1e9
 
-    # roofline of the persistent kernel (algorithmic bytes)
-    b_alg = 12 * R + 16 * (Wr + 1) + 12 * Wr
+    # the other schedule, timed the same way (Jacobi: deterministic counters = the oracle's;
+    # its R_J, W_J define the algorithmic bytes of the workload)
+    oflag = 0 if sflag else N.F_ASYNC
+    for _ in range(2):
+        step(flags=oflag)
+    ev2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+            torch.cuda.Event(enable_timing=True)) for _ in range(max(3, min(K, 20)))]
+    for e in ev2:
+        step(e, flags=oflag)
+    torch.cuda.synchronize()
+    o_kern = statistics.mean(b.elapsed_time(c) for a, b, c in ev2) / 1e3
+    o_step = statistics.mean(a.elapsed_time(c) for a, b, c in ev2) / 1e3
+    st2 = N.Stats()
+    N.check(L.dawn_solver_result(s, None, None, ctypes_byref(st2), stream))
+    if sflag:
+        RJ, WJ = int(st2.relaxations), int(st2.writes)
+    else:
+        RJ, WJ = R, Wr
+    other = {"schedule": "jacobi" if sflag else "async", "ms_per_step": 1e3 * o_step, "kernel_ms": 1e3 * o_kern,
+             "value": world * m_reach / o_step / 1e9, "unit": "GTEPS", "relaxations": int(st2.relaxations),
+             "writes": int(st2.writes), "rounds": int(st2.outer_steps)}
+
+    # roofline of the persistent kernel (algorithmic bytes):
+    # B_alg = 12 R_J + 16 (W_J + 1) + 12 W_J from the snapshot-Jacobi counts
+    b_alg = 12 * RJ + 16 * (WJ + 1) + 12 * WJ
+    b_act = 12 * R + 16 * (Wr + 1) + 12 * Wr  # the bytes this schedule's own work implies
     t_kern = statistics.mean(kern_ms) / 1e3
     peak, peak_src = hbm_peak()
     achieved = b_alg / t_kern / 1e9
@@ -433,7 +461,7 @@ def ours(args):
                                         N.F32, 0, C.byref(h)))
             sv = C.c_void_p()
             N.check(L.dawn_solver_create(h, 0, C.byref(sv)))
-            N.check(L.dawn_sssp(sv, src, N.GOVM, 0, out_h.data_ptr(), None, C.byref(st_e), stream))
+            N.check(L.dawn_sssp(sv, src, N.GOVM, sflag, out_h.data_ptr(), None, C.byref(st_e), stream))
             N.check(L.dawn_solver_destroy(sv))
             N.check(L.dawn_graph_destroy(h))
 
@@ -460,16 +488,17 @@ def ours(args):
         if not np.array_equal(np.isfinite(out_h.numpy()), fin.cpu().numpy()):
             raise AssertionError("C-ABI result disagrees with the timed device result")
         # resident graph through the Python API (upload cached, as the reference holds its CsrGraph)
-        P.govm_sssp(host, src, precision="fp32")
+        P.govm_sssp(host, src, precision="fp32", schedule=args.schedule)
         torch.cuda.synchronize()
         KR = max(3, min(K, 20))
         t0 = time.perf_counter()
         for _ in range(KR):
-            dv, _, _st = P.govm_sssp(host, src, precision="fp32")
+            dv, _, _st = P.govm_sssp(host, src, precision="fp32", schedule=args.schedule)
         t_res = (time.perf_counter() - t0) / KR
         e2e_resident = {"value": world * m_reach / t_res / 1e9, "unit": "GTEPS", "ms_per_step": 1e3 * t_res,
                         "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 8 * n + 48,
-                        "note": "P.govm_sssp(CsrGraph, 0, precision='fp32'), graph upload cached by identity"}
+                        "note": f"P.govm_sssp(CsrGraph, 0, precision='fp32', schedule='{args.schedule}'), graph "
+                                "upload cached by identity"}
         if not np.array_equal(np.isfinite(dv.dist), fin.cpu().numpy()):
             raise AssertionError("public-API result disagrees with the timed device result")
 
@@ -499,8 +528,16 @@ def ours(args):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "peak_source": peak_src, "kernel": "dawn_persistent<float,uint32,wide>",
                      "bytes_alg": b_alg, "kernel_ms": 1e3 * t_kern,
-                     "bytes_formula": "12*R + 16*(W+1) + 12*W (col+w+dist per relax; row_ptr+frontier per scan; "
-                                      "dist+frontier per write)"},
+                     "bytes_formula": "12*R_J + 16*(W_J+1) + 12*W_J with the snapshot-Jacobi counts R_J, W_J "
+                                      "(BASELINE.md §2; col+w+dist per relax, row_ptr+frontier per scan, "
+                                      "dist+frontier per write)",
+                     "achieved_own_work": b_act / t_kern / 1e9, "frac_own_work": b_act / t_kern / 1e9 / peak,
+                     "own_work_note": "the same formula with this schedule's own R, W"},
+        "schedule": {"headline": args.schedule,
+                     "note": "async: frontier rows relaxed with their live distance (as the reference's in-place "
+                             "order); identical distances, fewer relaxations, counters timing-dependent. jacobi: "
+                             "round-start snapshots, counters deterministic and equal to the oracle",
+                     "other": other},
         "cpu_baseline": cpu,
         "e2e": e2e,
         "e2e_resident": e2e_resident,

@@ -163,7 +163,7 @@ __device__ void phase_snapshot(const KParams<V, EI>& P, int p) {
   const EI* qo = P.qoff[p];
   for (uint32_t i = blockIdx.x * NT + threadIdx.x; i < cnt; i += gridDim.x * NT) {
     const uint32_t u = ldcg(qn + i);
-    P.qkey[p][i] = ldcg(P.dist + u);
+    if (!P.live) P.qkey[p][i] = ldcg(P.dist + u);  // the async schedule reads live values instead
     const EI off = ldcg(qo + i);
     const EI nxt = (i + 1 < cnt) ? ldcg(qo + i + 1) : E;
     mark_tiles<XI, EI>(P.tile_row, off, nxt - off, i);
@@ -314,7 +314,7 @@ __device__ void phase_compact(const KParams<V, EI>& P, int p, uint32_t r, Smem<V
           P.qnode[p][pos] = u0 + j;
           P.qoff[p][pos] = off;
           P.qbase[p][pos] = rp[j] - off;
-          P.qkey[p][pos] = keys[j];
+          if (!P.live) P.qkey[p][pos] = keys[j];
           mark_tiles<XI, EI>(P.tile_row, off, deg, pos);
           pos++;
           off += deg;
@@ -477,7 +477,7 @@ __device__ void phase_bitmap(const KParams<V, EI>& P, int p, uint32_t r, unsigne
           P.qnode[p][pos] = vv[h];
           P.qoff[p][pos] = off;
           P.qbase[p][pos] = aa[h] - off;
-          P.qkey[p][pos] = kk[h];
+          if (!P.live) P.qkey[p][pos] = kk[h];
           mark_tiles<XI, EI>(P.tile_row, off, bb[h] - aa[h], pos);
           pos++;
           off += bb[h] - aa[h];

@@ -18,6 +18,7 @@ if [[ $what == all || $what == bench ]]; then
   timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
   echo "bench rc=$?"; tail -c 600 gpurun_out/bench.json; tail -3 gpurun_out/bench.err
   timeout 600 python tools/round_profile.py --solves 5 --out gpurun_out/rounds_c2.json > gpurun_out/rounds_c2.txt 2>&1
+  timeout 600 python tools/round_profile.py --solves 5 --schedule jacobi > gpurun_out/rounds_c2_jacobi.txt 2>&1
   timeout 600 python tools/apsp_probe.py --k 512 --single 8 > gpurun_out/rounds_c3.txt 2>&1
 fi
 if [[ $what == all || $what == ncu ]]; then

@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--grid", type=int, default=0, help="grid side (>0: 2D grid instead of RMAT)")
     ap.add_argument("--dense", type=float, default=None, help="dense_edges_per_node tuning knob")
     ap.add_argument("--bitmap", type=float, default=None, help="bitmap_edges_per_node tuning knob")
+    ap.add_argument("--schedule", choices=["async", "jacobi"], default="async")
     ap.add_argument("--tune", action="append", default=[], help="key=value solver tuning (repeatable)")
     a = ap.parse_args()
     import torch
@@ -58,7 +59,7 @@ def main():
     for _ in range(a.solves):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        N.check(L.dawn_sssp_begin(s, a.source, algo, 0, stream))
+        N.check(L.dawn_sssp_begin(s, a.source, algo, N.F_ASYNC if a.schedule == "async" else 0, stream))
         N.check(L.dawn_sssp_run(s, 0, stream))
         e1.record()
         torch.cuda.synchronize()
