@@ -2,7 +2,8 @@
 # One GPU round trip: parity tests, bench, launch list, ncu captures of the
 # persistent single-source kernel (C2) and the batched kernel (C3), per-round
 # timelines.  Run under gpurun from the repo root:
-#   gpurun --timeout 2400 -- 'bash tools/gpu_check.sh [tests|bench|ncu|all]'
+#   gpurun --timeout 2400 -- 'bash tools/gpu_check.sh [tests|bench|ncu|ncu_c2|ncu_batch|all]'
+# (ncu = both captures; together they can exceed gpurun's 64 MiB return limit)
 set -u
 what=${1:-all}
 mkdir -p gpurun_out
@@ -21,13 +22,15 @@ if [[ $what == all || $what == bench ]]; then
   timeout 600 python tools/round_profile.py --solves 5 --schedule jacobi > gpurun_out/rounds_c2_jacobi.txt 2>&1
   timeout 600 python tools/apsp_probe.py --k 512 --single 8 > gpurun_out/rounds_c3.txt 2>&1
 fi
-if [[ $what == all || $what == ncu ]]; then
+if [[ $what == all || $what == ncu || $what == ncu_c2 ]]; then
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
     python bench.py --steps 3 --warmup 3 --no-cpu-baseline --apsp-sources 256 > gpurun_out/ncu_bench.log 2>&1
   echo "ncu launches rc=$?"
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:dawn_persistent -s 2 -c 1 \
     -o gpurun_out/prof_c2 -f python tools/round_profile.py --solves 3 > gpurun_out/ncu_full.log 2>&1
   echo "ncu c2 rc=$?"
+fi
+if [[ $what == all || $what == ncu || $what == ncu_batch ]]; then
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:dawn_batch_persistent -s 3 -c 1 \
     -o gpurun_out/prof_batch -f python tools/apsp_probe.py --k 128 --single 2 > gpurun_out/ncu_batch.log 2>&1
   echo "ncu batch rc=$?"
