@@ -526,7 +526,7 @@ def ours(args):
         "config": workload_config(args, {"l2": "flushed between steps (256 MiB write outside the timed events)",
                                          "precision": "fp32 (opt-in, <=1e-6 relative vs the fp64 reference)"}),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "peak_source": peak_src, "kernel": "dawn_persistent<float,uint32,wide>",
+                     "traffic": traffic, "peak_source": peak_src, "kernel": "dawn_persistent<float,uint32,wide>" + (" + dawn_worklist tail" if sflag else ""),
                      "bytes_alg": b_alg, "kernel_ms": 1e3 * t_kern,
                      "bytes_formula": "12*R_J + 16*(W_J+1) + 12*W_J with the snapshot-Jacobi counts R_J, W_J "
                                       "(BASELINE.md §2; col+w+dist per relax, row_ptr+frontier per scan, "
@@ -542,7 +542,8 @@ def ours(args):
         "e2e": e2e,
         "e2e_resident": e2e_resident,
         "apsp": apsp,
-        "gpu_launches": 2 * K,
+        # per step: dawn_init_solve + dawn_persistent (+ dawn_worklist under the async schedule)
+        "gpu_launches": (3 if sflag else 2) * K,
         "clocks": clocks,
         "relax_gps": world * R / t_step / 1e9,
         "solve": {"rounds": steps_run, "relaxations": R, "writes": Wr, "first_discoveries": int(st.first_discoveries),

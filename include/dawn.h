@@ -128,7 +128,13 @@ int dawn_solver_destroy(dawn_solver_t s);
  *   m >= 2^25 and m >= 8n.
  *   "bitmap_frontier" (default -1 = auto): 1 / 0 forces / disables the
  *   bitmap frontier of light rounds (auto: average out-degree < 8 and
- *   n >= 4096, narrow tiles; never with predecessors). */
+ *   n >= 4096, narrow tiles; never with predecessors).
+ *   "worklist_edges" (default 2^17; 0 = off): under DAWN_F_ASYNC, on graphs
+ *   without negative weights, GOVM, unbounded runs, once a round relaxes
+ *   fewer edges than this the rest of the solve runs barrier-free (a ring of
+ *   row items taken by all warps).  Distances, negative_cycle and
+ *   first_discoveries are unchanged; outer_steps reports the round at which
+ *   the worklist took over. */
 int dawn_solver_tune(dawn_solver_t s, const char* key, double value);
 
 /* One single-source solve: govm_sssp / gsvm_sssp (solver.py:265-399),

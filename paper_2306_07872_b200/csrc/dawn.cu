@@ -87,6 +87,10 @@ struct dawn_solver_s {
   void* qbase[2] = {nullptr, nullptr};
   void* qkey[2] = {nullptr, nullptr};
   uint32_t* tile_row = nullptr;
+  unsigned long long* wl_ring = nullptr;  // worklist tail (graphs without negative weights)
+  uint64_t wl_cap = 0;
+  int wl_grid = 1;
+  double worklist_edges = 1 << 17;        // tunable: async rounds relaxing < this many edges end the solve barrier-free (0 = off)
   DevState* st = nullptr;
   DevState* st_host = nullptr;  // pinned
   double* dbuf = nullptr;
@@ -452,6 +456,9 @@ struct Impl {
     P.prof_cap = s->prof_cap;
     P.cta_prof = s->cta_prof;
     P.live = (s->run_flags & DAWN_F_ASYNC) && !P.pred_on ? 1 : 0;
+    P.wl_ring = s->worklist_edges > 0 ? s->wl_ring : nullptr;
+    P.wl_mask = s->wl_cap ? s->wl_cap - 1 : 0;
+    P.wl_edges = (unsigned long long)s->worklist_edges;
     return P;
   }
 
@@ -508,6 +515,9 @@ struct Impl {
     s->grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)bps0 * nsm, work));
     s->grid_pred = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)bps1 * nsm, work));
     s->smem = sm;
+    int bpw = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpw, dawn_worklist<V, EI>, NT, 0));
+    s->wl_grid = std::max(1, bpw) * nsm;
     return DAWN_OK;
   }
 
@@ -532,6 +542,11 @@ struct Impl {
     void* fn = kernel_for(s, P.pred_on != 0);
     CK(cudaLaunchCooperativeKernel(fn, dim3(P.pred_on ? s->grid_pred : s->grid), dim3(NT), args, s->smem,
                                    stream));
+    // the worklist tail, when the persistent kernel handed over (it returns at once otherwise)
+    if (P.wl_ring && P.live && P.algo == 0 && max_rounds == 0xFFFFFFFFu && !s->g->has_negative && !s->fb) {
+      dawn_worklist<V, EI><<<s->wl_grid, NT, 0, stream>>>(P);
+      CK(cudaGetLastError());
+    }
     return DAWN_OK;
   }
 
@@ -674,7 +689,17 @@ struct Impl {
     CK(cudaMalloc(&s->dist, ks * n));
     CK(cudaMalloc(&s->stamp, 4 * n));
     CK(cudaMalloc(&s->bmap, 4 * (size_t)((n + 31) / 32 + 4)));  // padded for 16-byte loads
-    CK(cudaMalloc(&s->wstate, (size_t)n));
+    CK(cudaMalloc(&s->wstate, (size_t)n + 4));  // + 4: the worklist tail updates it by 32-bit words
+    if (!s->g->has_negative) {
+      // worklist tail (async schedule): ring of items (every node once + long-row chunks + slack;
+      // a full ring only makes producers wait)
+      const uint64_t need = (uint64_t)n + (uint64_t)(m / WT_MIN) + (1ull << 16);
+      uint64_t cap = 1;
+      while (cap < need) cap <<= 1;
+      s->wl_cap = cap;
+      CK(cudaMalloc(&s->wl_ring, 16 * cap));  // 16-byte items; node field 0xFFFFFFFF = empty
+      CK(cudaMemset(s->wl_ring, 0xFF, 16 * cap));
+    }
     if (s->flags & (DAWN_F_PRED | DAWN_F_NEGCHECK)) {
       CK(cudaMalloc(&s->pred, 8 * n));
       CK(cudaMalloc(&s->jmp0, 4 * n));
@@ -734,6 +759,7 @@ static void solver_free(dawn_solver_t s) {
     cudaFree(s->qkey[i]);
   }
   cudaFree(s->tile_row);
+  cudaFree(s->wl_ring);
   cudaFree(s->st);
   cudaFreeHost(s->st_host);
   cudaFree(s->dbuf);
@@ -778,6 +804,11 @@ extern "C" int dawn_solver_tune(dawn_solver_t s, const char* key, double value) 
   if (!strcmp(key, "dense_edges_per_node")) {
     if (!(value >= 0.0)) return fail(DAWN_EINVAL, "dense_edges_per_node must be >= 0");
     s->dense_edges_per_node = value;
+    return DAWN_OK;
+  }
+  if (!strcmp(key, "worklist_edges")) {
+    if (!(value >= 0.0)) return fail(DAWN_EINVAL, "worklist_edges must be >= 0");
+    s->worklist_edges = value;
     return DAWN_OK;
   }
   if (!strcmp(key, "wide_tiles")) {

@@ -67,6 +67,11 @@ struct KParams {
   unsigned prof_cap;                   // rounds the timeline can hold
   unsigned long long* cta_prof;        // debug: per-CTA S/X work end times [round][2][grid], or nullptr
   int live;                            // async schedule: frontier rows relaxed with their live value (no snapshot)
+  // worklist tail (async schedule, non-negative weights, unbounded run): once a
+  // round relaxes < wl_edges edges the rest of the solve runs barrier-free
+  unsigned long long* wl_ring;         // ring of 16-byte row items (uint4); nullptr = off
+  unsigned long long wl_mask;          // ring capacity - 1 (power of two)
+  unsigned long long wl_edges;
 };
 
 constexpr int WPB = NT / 32;       // warps per CTA
@@ -771,6 +776,330 @@ __device__ void phase_expand(const KParams<V, EI>& P, int p, uint32_t r, bool de
 
 
 // ---------------------------------------------------------------------------
+// Worklist tail (async schedule only; graphs without negative weights; a run
+// without a round limit).  The last rounds of an RMAT solve relax ~1 % of the
+// edges but cost ~15 % of the time: a round is a chain of ~10 dependent global
+// accesses plus two grid barriers (~20 us) however few rows it has.  Once a
+// round relaxes fewer than wl_edges edges, the rest of the solve runs
+// barrier-free (dawn_worklist, launched behind the persistent kernel) off a
+// ring of 16-byte row items {node, degree, first edge, value}:
+//   * a relax that lowers dist[v] pushes v's row carrying the value it wrote
+//     (no re-read of dist[v], no queued flag: the item itself is the message);
+//     rows longer than CH = 32*XI edges travel as one split item that the warp
+//     taking it turns into one item per CH-edge chunk;
+//   * a warp claims up to 32 consecutive ring slots (fewer when the queue is
+//     short), takes whichever are filled and relaxes their rows together as
+//     one virtual edge list cut into warp tiles (the X phase's <= 32-row tile);
+//     an item whose value is no longer dist[v] is dropped (a lower write
+//     pushed its own item);
+//   * one 64-bit counter carries (pending items << 32 | ring tail): a push
+//     adds (k << 32 | k) before its items become visible; a warp retires the
+//     items it took with one subtraction after its own pushes, so
+//     pending == 0 is final.
+// Why the result is the reference's: every candidate is fl(d + w) for a value
+// d that dist[u] held, values only decrease, and every lowering pushes an item
+// whose relax uses the value written, so the run stops only at the greatest
+// fixpoint the snapshot rounds reach (the async argument).
+// first_discoveries is exact (the unique atomicMin that returned INF); writes,
+// nodes lowered twice and relaxations are this run's own.
+// ---------------------------------------------------------------------------
+constexpr uint32_t WL_NONE = 0xFFFFFFFFu;   // empty slot (node field)
+constexpr uint32_t WL_SPLIT = 0xFFFFFFFFu;  // degree field: the whole long row (split when taken)
+constexpr uint32_t WL_CHUNK = 0x80000000u;  // degree field: chunk index of a long row
+
+__device__ __forceinline__ unsigned long long wl_retire(unsigned n) { return 0ull - ((unsigned long long)n << 32); }
+
+__device__ __forceinline__ uint4 ld_relaxed_v4(const uint4* p) {
+  uint4 v;
+  asm volatile("ld.relaxed.gpu.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_v4(uint4* p, uint4 v) {
+  asm volatile("st.relaxed.gpu.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// item layout: x = node, y = degree / WL_SPLIT / WL_CHUNK|chunk, z,w = value key (64-bit)
+template <class K>
+__device__ __forceinline__ uint4 wl_item(uint32_t node, uint32_t y, K key) {
+  const unsigned long long k = (unsigned long long)key;
+  return make_uint4(node, y, (uint32_t)k, (uint32_t)(k >> 32));
+}
+
+// store an item into a reserved slot; waits only if the slot's previous item
+// (one lap back) has not been taken yet
+__device__ __forceinline__ void wl_store(uint4* q, uint32_t pre_node, uint4 item) {
+  unsigned long long t0 = 0;
+  while (pre_node != WL_NONE) {
+    __nanosleep(64);
+    pre_node = ld_relaxed_u32(&q->x);
+    const unsigned long long t = globaltimer();
+    if (t0 == 0) t0 = t;
+    else if (t - t0 > 30ull * 1000000000ull) asm volatile("trap;");
+  }
+  st_relaxed_v4(q, item);
+}
+
+// push the rows of node[j] (mask msk, degree deg[j]) with the values key[j]
+// this lane wrote.  Warp-collective.
+template <class V, class EI, int NJ, class K>
+__device__ __forceinline__ void wl_push(const KParams<V, EI>& P, const uint32_t (&node)[NJ],
+                                        const uint32_t (&deg)[NJ], const K (&key)[NJ], unsigned msk, uint32_t CH) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t mine = __popc(msk);
+  const uint32_t incl = warp_incl_sum<uint32_t>(mine);
+  const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+  if (tot == 0) return;
+  unsigned long long base = 0;
+  if (lane == 0) base = atomicAdd(&P.st->wl_ctr, ((unsigned long long)tot << 32) | tot);
+  const uint32_t slot0 = (uint32_t)__shfl_sync(0xffffffffu, base, 0) + incl - mine;
+  uint4* ring = reinterpret_cast<uint4*>(P.wl_ring);
+  uint32_t pre[NJ];
+  uint32_t t = 0;
+#pragma unroll
+  for (int j = 0; j < NJ; ++j)  // all lap checks in flight at once
+    if ((msk >> j) & 1u) pre[j] = ld_relaxed_u32(&ring[(slot0 + t++) & P.wl_mask].x);
+  t = 0;
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) {
+    if ((msk >> j) & 1u) {
+      uint4* q = ring + ((slot0 + t++) & P.wl_mask);
+      wl_store(q, pre[j], wl_item<K>(node[j], deg[j] > CH ? WL_SPLIT : deg[j], key[j]));
+    }
+  }
+}
+
+// relax edges [e0, e0 + len) (len <= 32*XI) of the rows held in lanes 0..nb-1
+// (first virtual edge off_k ascending, first real edge a_k, value val_k, every
+// row non-empty) and push the rows they lower.  Warp-collective.
+template <class V, class EI, int XI>
+__device__ __forceinline__ void wl_relax_tile(const KParams<V, EI>& P, uint32_t nb, uint32_t off, EI a,
+                                              typename Codec<V, true>::C val, uint32_t e0, uint32_t len,
+                                              unsigned long long& acc_w, unsigned long long& acc_fd,
+                                              unsigned long long& acc_multi) {
+  using CD = Codec<V, true>;
+  using K = typename CD::K;
+  using WB = typename CD::WB;
+  using C = typename CD::C;
+  constexpr uint32_t CH = 32 * XI;
+  const uint32_t lane = threadIdx.x & 31;
+  // rows starting at or before e0: the last of them holds e0
+  const uint32_t i0 = __popc(__ballot_sync(0xffffffffu, lane < nb && off <= e0)) - 1;
+  const uint32_t rst = (lane < nb && lane >= i0) ? (off > e0 ? off - e0 : 0u) : 0xFFFFFFFFu;
+  uint32_t col[XI];
+  WB wv[XI];
+  C rv[XI];
+  unsigned okm = 0;
+  uint32_t before = 0;
+#pragma unroll
+  for (int j = 0; j < XI; ++j) {
+    const uint32_t lo = j * 32;
+    const uint32_t bit = (rst - lo < 32u) ? (1u << (rst - lo)) : 0u;
+    const uint32_t B = __reduce_or_sync(0xffffffffu, bit);
+    const uint32_t k = i0 + before + __popc(B & (0xFFFFFFFFu >> (31 - lane))) - 1;
+    before += __popc(B);
+    const uint32_t x = e0 + lo + lane;
+    const EI pos = __shfl_sync(0xffffffffu, a, k) + (EI)(x - __shfl_sync(0xffffffffu, off, k));
+    rv[j] = __shfl_sync(0xffffffffu, val, k);
+    okm |= (unsigned)(lo + lane < len) << j;
+    if (lo + lane < len) EdgeAccess<V>::load(P, pos, col[j], wv[j]);
+    else { col[j] = 0; wv[j] = 0; }
+  }
+  K cand[XI];
+#pragma unroll
+  for (int j = 0; j < XI; ++j) {
+    cand[j] = CD::relax(rv[j], wv[j]);
+    if (!CD::usable(cand[j])) okm &= ~(1u << j);
+  }
+  // gathers and the lowered rows' bounds in flight together
+  K cur[XI];
+  EI ra[XI], rb[XI];
+#pragma unroll
+  for (int j = 0; j < XI; ++j) {
+    const bool ok = (okm >> j) & 1u;
+    cur[j] = ok ? ldcg(P.dist + col[j]) : (K)0;
+    ra[j] = ok ? __ldg(P.row_ptr + col[j]) : (EI)0;
+    rb[j] = ok ? __ldg(P.row_ptr + col[j] + 1) : (EI)0;
+  }
+  unsigned low = 0;
+  uint32_t dg[XI];
+#pragma unroll
+  for (int j = 0; j < XI; ++j) {
+    dg[j] = (uint32_t)(rb[j] - ra[j]);
+    if (((okm >> j) & 1u) && cand[j] < cur[j]) {
+      if (col[j] == P.src) { P.st->flag = 1u; continue; }
+      const uint32_t v = col[j];
+      unsigned* wsw = reinterpret_cast<unsigned*>(P.wstate + (v & ~3u));
+      const unsigned sh = 8u * (v & 3u);
+      bool lowered = true;
+      if (cur[j] == CD::INF) {  // maybe the first discovery: it must be counted exactly once
+        const K old = atomicMin(P.dist + v, cand[j]);
+        lowered = cand[j] < old;
+        if (old == CD::INF) { acc_fd++; atomicOr(wsw, 1u << sh); }
+        else if (lowered && !(atomicOr(wsw, 2u << sh) & (2u << sh))) acc_multi++;
+      } else {
+        atomicMin(P.dist + v, cand[j]);  // fire and forget: cand < cur means it lowered dist[v] or a
+                                         // racing write went lower (then this item is dropped as stale)
+        if (!(atomicOr(wsw, 2u << sh) & (2u << sh))) acc_multi++;
+      }
+      if (lowered) {
+        acc_w++;
+        if (dg[j] > 0) low |= 1u << j;
+      }
+    }
+  }
+  wl_push<V, EI, XI, K>(P, col, dg, cand, low, CH);
+}
+
+// round r's frontier (queue p) becomes the first items; the persistent kernel
+// then exits and dawn_worklist (launched behind it) takes over
+template <class V, class EI>
+__device__ void wl_seed(const KParams<V, EI>& P, int p) {
+  using K = typename Codec<V, true>::K;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t gw = (blockIdx.x * NT + threadIdx.x) >> 5, nw = gridDim.x * WPB;
+  const uint32_t cnt = (uint32_t)pk_count(ldcg(&P.st->res[p]), P.ebits);
+  for (uint32_t b0 = gw * 32; b0 < cnt; b0 += nw * 32) {
+    const bool ok = b0 + lane < cnt;
+    uint32_t v[1] = {ok ? ldcg(P.qnode[p] + b0 + lane) : 0u};
+    K key[1] = {ok ? ldcg(P.dist + v[0]) : (K)0};
+    uint32_t dg[1] = {ok ? (uint32_t)(__ldg(P.row_ptr + v[0] + 1) - __ldg(P.row_ptr + v[0])) : 0u};
+    wl_push<V, EI, 1, K>(P, v, dg, key, (ok && dg[0] > 0) ? 1u : 0u, 32u * XI_NARROW);
+  }
+}
+
+template <class V, class EI>
+__global__ void __launch_bounds__(NT, 2) dawn_worklist(KParams<V, EI> P) {
+  constexpr int XI = XI_NARROW;
+  using CD = Codec<V, true>;
+  using K = typename CD::K;
+  using C = typename CD::C;
+  constexpr uint32_t CH = 32 * XI;
+  DevState* st = P.st;
+  if (ldcg(&st->wl_mode) == 0u) return;  // the solve finished in rounds
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t nw = gridDim.x * WPB;
+  uint4* ring = reinterpret_cast<uint4*>(P.wl_ring);
+  unsigned long long acc_w = 0, acc_fd = 0, acc_multi = 0, acc_e = 0, acc_i = 0;
+  unsigned own = 0;  // claimed slots h + lane not taken yet
+  uint32_t h = 0;
+  unsigned ns = 32;
+  unsigned long long t0 = 0;
+  for (;;) {
+    if (own == 0) {
+      uint32_t c = 1;
+      if (lane == 0) {
+        const uint32_t tail = (uint32_t)ld_relaxed(&st->wl_ctr), head = (uint32_t)ld_relaxed(&st->wl_head);
+        const uint32_t avail = tail - head;
+        c = (avail < 0x80000000u) ? min(32u, max(1u, avail / nw)) : 1u;
+        h = (uint32_t)atomicAdd(&st->wl_head, (unsigned long long)c);
+      }
+      c = __shfl_sync(0xffffffffu, c, 0);
+      h = __shfl_sync(0xffffffffu, h, 0);
+      own = (c >= 32) ? 0xFFFFFFFFu : ((1u << c) - 1u);
+    }
+    uint4* q = ring + ((h + lane) & P.wl_mask);
+    uint4 it = make_uint4(WL_NONE, WL_NONE, WL_NONE, WL_NONE);
+    if ((own >> lane) & 1u) it = ld_relaxed_v4(q);
+    // filled = both 8-byte halves written (w, the key's high word, is <= 0x7FFFFFFF in a real item)
+    const unsigned got = __ballot_sync(0xffffffffu, it.x != WL_NONE && it.w != WL_NONE);
+    if (got == 0) {
+      bool fin = false;
+      if (lane == 0) {
+        fin = (ld_relaxed(&st->wl_ctr) >> 32) == 0ull;
+        const unsigned long long t = globaltimer();
+        if (t0 == 0) t0 = t;
+        else if (t - t0 > 30ull * 1000000000ull) asm volatile("trap;");
+      }
+      if (__shfl_sync(0xffffffffu, fin, 0)) break;
+      __nanosleep(ns);
+      if (ns < 256) ns <<= 1;
+      continue;
+    }
+    ns = 32;
+    t0 = 0;
+    own &= ~got;
+    const bool mine = (got >> lane) & 1u;
+    if (mine) st_relaxed_v4(q, make_uint4(WL_NONE, WL_NONE, WL_NONE, WL_NONE));
+    const uint32_t u = it.x, y = it.y;
+    const K key = (K)(((unsigned long long)it.w << 32) | it.z);
+    // single-chunk rows: first edge and the stale check (a lower value was pushed separately)
+    EI a = 0;
+    K now = key;
+    const bool single = mine && y <= CH;
+    if (single) {
+      a = __ldg(P.row_ptr + u);
+      now = ldcg(P.dist + u);
+    }
+    // drop only an item whose value was undercut (a lower write pushed its own item); a value above
+    // the item's means the item's own fire-and-forget min has not landed yet
+    const unsigned sm = __ballot_sync(0xffffffffu, single && !(now < key));
+    if (sm) {
+      const uint32_t nb = __popc(sm);
+      const uint32_t fl = (lane < nb) ? __fns(sm, 0, lane + 1) : 0u;
+      const EI ra = __shfl_sync(0xffffffffu, a, fl);
+      const uint32_t rd = __shfl_sync(0xffffffffu, y, fl);
+      const K rk = __shfl_sync(0xffffffffu, key, fl);
+      const uint32_t rdeg = (lane < nb) ? rd : 0u;
+      const uint32_t incl = warp_incl_sum<uint32_t>(rdeg);
+      const uint32_t Eb = __shfl_sync(0xffffffffu, incl, 31);
+      const uint32_t off = incl - rdeg;
+      const C val = CD::dec(rk);
+      for (uint32_t e0 = 0; e0 < Eb; e0 += CH)
+        wl_relax_tile<V, EI, XI>(P, nb, off, ra, val, e0, min(CH, Eb - e0), acc_w, acc_fd, acc_multi);
+      if (lane == 0) acc_e += Eb;
+    }
+    // long rows: split items and chunks, one at a time
+    unsigned lm = __ballot_sync(0xffffffffu, mine && y > CH);
+    while (lm) {
+      const int l = __ffs(lm) - 1;
+      lm &= lm - 1;
+      const uint32_t lu = __shfl_sync(0xffffffffu, u, l), ly = __shfl_sync(0xffffffffu, y, l);
+      const K lk = __shfl_sync(0xffffffffu, key, l);
+      const EI la = __ldg(P.row_ptr + lu), lb = __ldg(P.row_ptr + lu + 1);
+      if (ldcg(P.dist + lu) < lk) continue;  // undercut: a lower write pushed its own item
+      if (ly == WL_SPLIT) {
+        const uint32_t nch = (uint32_t)((lb - la + (EI)CH - 1) / (EI)CH);
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(&st->wl_ctr, ((unsigned long long)nch << 32) | nch);
+        const uint32_t b0 = (uint32_t)__shfl_sync(0xffffffffu, base, 0);
+        for (uint32_t c = lane; c < nch; c += 32) {
+          uint4* qq = ring + ((b0 + c) & P.wl_mask);
+          wl_store(qq, ld_relaxed_u32(&qq->x), wl_item<K>(lu, WL_CHUNK | c, lk));
+        }
+        __syncwarp();
+      } else {
+        const EI e0 = la + (EI)(ly & ~WL_CHUNK) * (EI)CH;
+        const uint32_t len = (lb - e0 < (EI)CH) ? (uint32_t)(lb - e0) : CH;
+        wl_relax_tile<V, EI, XI>(P, 1u, 0u, e0, CD::dec(lk), 0u, len, acc_w, acc_fd, acc_multi);
+        if (lane == 0) acc_e += len;
+      }
+    }
+    __syncwarp();
+    if (lane == 0) {
+      acc_i += __popc(got);
+      atomicAdd(&st->wl_ctr, wl_retire(__popc(got)));  // after this warp's pushes
+    }
+  }
+  acc_w = warp_sum_u64(acc_w);
+  acc_fd = warp_sum_u64(acc_fd);
+  acc_multi = warp_sum_u64(acc_multi);
+  if (lane == 0) {
+    if (acc_e) atomicAdd(&st->R, acc_e);
+    if (acc_i) atomicAdd(&st->wl_items, acc_i);
+    if (acc_w) atomicAdd(&st->W, acc_w);
+    if (acc_fd) atomicAdd(&st->FD, acc_fd);
+    if (acc_multi) atomicAdd(&st->multi, acc_multi);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Negative-cycle early exit: a cycle in the predecessor graph (each finite
 // node -> the frontier node that produced its value in its last lowering
 // round) implies a reachable negative cycle when arithmetic is exact
@@ -893,11 +1222,25 @@ __global__ void __launch_bounds__(NT, DAWN_MIN_BLOCKS) dawn_persistent(KParams<V
     // ---- X phase ----
     const unsigned long long E = pk_edges(ldcg(&st->res[p]), P.ebits);
     const bool dense = P.algo == 1 || E >= P.dense_edges;
-    if (leader) acc_r += E;  // relaxations (solver.py:297, :372)
     if (prof) {
       P.prof[4 * r + 1] = globaltimer();
       P.prof[4 * r + 3] = ldcg(&st->res[p]);
     }
+    if constexpr (RAW && !WITH_PRED && !FB) {
+      if (P.wl_ring != nullptr && P.live && P.algo == 0 && P.max_rounds == 0xFFFFFFFFu && r >= 2 &&
+          E < P.wl_edges) {
+        wl_seed<V, EI>(P, p);
+        if (prof) P.prof[4 * r + 2] = globaltimer();  // the seeding; dawn_worklist runs after
+        if (leader) {
+          st->wl_mode = 1u;
+          st->steps = r;
+          st->done = 1u;
+          st->round = r + 1;
+        }
+        break;
+      }
+    }
+    if (leader) acc_r += E;  // relaxations (solver.py:297, :372)
     uint32_t round_w = 0;
     phase_expand<V, EI, false, RAW, XI, FB>(P, p, r, dense, s, acc_w, acc_fd, acc_multi, round_w);
     round_w = __reduce_add_sync(0xffffffffu, round_w);
@@ -957,6 +1300,8 @@ __global__ void dawn_init_solve(KParams<V, EI> P) {
     st->cyc = 0u;
     st->steps = 0ull;
     st->R = st->W = st->FD = st->multi = 0ull;
+    st->wl_head = st->wl_ctr = st->wl_items = 0ull;
+    st->wl_mode = 0u;
   }
 }
 

@@ -86,6 +86,9 @@ def main():
         rate = x["edges"] / (x["x_us"] * 1e3) if x["x_us"] > 0 else 0
         print(f"{x['round']:>4} {x['entries']:>10} {x['edges']:>12} {x['s_us']:>8.1f} {x['x_us']:>9.1f} {rate:>8.1f}")
     print(f"sum S {tot_s:.1f} us, sum X {tot_x:.1f} us")
+    if rows and times:
+        tail = min(times) * 1e3 - (buf[4 * rows[-1]["round"] + 2] - buf[4 * rows[0]["round"]]) / 1e3
+        print(f"after the last recorded round (worklist kernel, if it ran, + launch gaps): {tail:.1f} us of the fastest solve")
     # per-CTA end of S / X work relative to the phase start (imbalance vs throughput)
     gridc = ctypes.c_int(0)
     cp = (ctypes.c_uint64 * (2 * 2048 * 64))()
