@@ -181,6 +181,11 @@ int dawn_solver_round_profile(dawn_solver_t s, uint64_t* out, int64_t cap_rounds
  * S and X work of the first 64 rounds of the last solve, before each phase's
  * grid barrier: out[(round * 2 + phase) * grid + cta], grid in *grid_out. */
 int dawn_solver_cta_profile(dawn_solver_t s, uint64_t* out, int64_t cap_rounds, int* grid_out, void* stream);
+/* Worklist tail of the last solve (all zero if the solve finished in rounds):
+ * out[0] = round handed over, [1] items taken, [2] warp batches, [3] / [4]
+ * warp-ns busy / waiting (sums over warps), [5] kernel span in ns.
+ * Synchronises `stream`. */
+int dawn_solver_worklist_stats(dawn_solver_t s, uint64_t* out, void* stream);
 
 /* Multi-source: independent solves from sources[0..k) (host int64 array) in
  * the given order — mssp (solver.py:426-457).  Uses the batched kernel

@@ -55,6 +55,7 @@ EXPORTS = (
     "dawn_solver_result",
     "dawn_solver_round_profile",
     "dawn_solver_cta_profile",
+    "dawn_solver_worklist_stats",
     "dawn_mssp",
     "dawn_batch_supported",
     "dawn_mssp_batch",
@@ -103,6 +104,7 @@ def _declare(L: ctypes.CDLL) -> None:
         "dawn_solver_result": (c_int, [c_void_p, c_void_p, c_void_p, POINTER(Stats), c_void_p]),
         "dawn_solver_round_profile": (c_int, [c_void_p, c_void_p, c_int64, P64, c_void_p]),
         "dawn_solver_cta_profile": (c_int, [c_void_p, c_void_p, c_int64, POINTER(c_int), c_void_p]),
+        "dawn_solver_worklist_stats": (c_int, [c_void_p, c_void_p, c_void_p]),
         "dawn_mssp": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_uint, c_void_p, c_void_p, c_void_p]),
         "dawn_batch_supported": (c_int, [c_void_p, c_int, c_uint, POINTER(c_int)]),
         "dawn_mssp_batch": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_uint, c_void_p, c_int, c_int64,

@@ -982,6 +982,23 @@ extern "C" int dawn_solver_cta_profile(dawn_solver_t s, uint64_t* out, int64_t c
   return DAWN_OK;
 }
 
+extern "C" int dawn_solver_worklist_stats(dawn_solver_t s, uint64_t* out, void* stream) {
+  if (!s || !out) return fail(DAWN_EINVAL, "NULL argument");
+  if (!s->active) return fail(DAWN_EINVAL, "no active solve");
+  cudaStream_t st = (cudaStream_t)stream;
+  CK(cudaSetDevice(s->g->device));
+  TRY(read_state(s, st));
+  const DevState& d = *s->st_host;
+  const bool ran = d.wl_mode != 0u;
+  out[0] = ran ? d.steps : 0;
+  out[1] = ran ? d.wl_items : 0;
+  out[2] = ran ? d.wl_batches : 0;
+  out[3] = ran ? d.wl_busy_ns : 0;
+  out[4] = ran ? d.wl_wait_ns : 0;
+  out[5] = (ran && d.wl_t1 > d.wl_t0) ? d.wl_t1 - d.wl_t0 : 0;
+  return DAWN_OK;
+}
+
 static bool batch_ok(dawn_solver_t s, int algo, unsigned flags) {
   return !s->g->has_negative && s->g->n >= 2 && !(flags & DAWN_F_PRED) && (algo == DAWN_GOVM || algo == DAWN_GSVM);
 }

@@ -312,6 +312,7 @@ struct DevState {
   alignas(128) unsigned long long wl_ctr;   // (items pushed and not yet retired << 32) | next ring slot to reserve
   unsigned long long wl_items;              // items taken (statistics)
   unsigned wl_mode;                         // the persistent kernel handed the solve to dawn_worklist
+  unsigned long long wl_batches, wl_busy_ns, wl_wait_ns, wl_t0, wl_t1;  // worklist timeline (sums over warps)
 };
 
 }  // namespace dawn

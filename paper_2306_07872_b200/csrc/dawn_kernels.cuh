@@ -987,6 +987,8 @@ __global__ void __launch_bounds__(NT, 2) dawn_worklist(KParams<V, EI> P) {
   const uint32_t nw = gridDim.x * WPB;
   uint4* ring = reinterpret_cast<uint4*>(P.wl_ring);
   unsigned long long acc_w = 0, acc_fd = 0, acc_multi = 0, acc_e = 0, acc_i = 0;
+  const unsigned long long t_begin = globaltimer();
+  unsigned long long busy = 0, nbatch = 0;
   unsigned own = 0;  // claimed slots h + lane not taken yet
   uint32_t h = 0;
   unsigned ns = 32;
@@ -1024,6 +1026,7 @@ __global__ void __launch_bounds__(NT, 2) dawn_worklist(KParams<V, EI> P) {
     }
     ns = 32;
     t0 = 0;
+    const unsigned long long t_got = globaltimer();
     own &= ~got;
     const bool mine = (got >> lane) & 1u;
     if (mine) st_relaxed_v4(q, make_uint4(WL_NONE, WL_NONE, WL_NONE, WL_NONE));
@@ -1085,8 +1088,11 @@ __global__ void __launch_bounds__(NT, 2) dawn_worklist(KParams<V, EI> P) {
     if (lane == 0) {
       acc_i += __popc(got);
       atomicAdd(&st->wl_ctr, wl_retire(__popc(got)));  // after this warp's pushes
+      busy += globaltimer() - t_got;
+      nbatch++;
     }
   }
+  const unsigned long long t_end = globaltimer();
   acc_w = warp_sum_u64(acc_w);
   acc_fd = warp_sum_u64(acc_fd);
   acc_multi = warp_sum_u64(acc_multi);
@@ -1096,6 +1102,11 @@ __global__ void __launch_bounds__(NT, 2) dawn_worklist(KParams<V, EI> P) {
     if (acc_w) atomicAdd(&st->W, acc_w);
     if (acc_fd) atomicAdd(&st->FD, acc_fd);
     if (acc_multi) atomicAdd(&st->multi, acc_multi);
+    atomicAdd(&st->wl_batches, nbatch);
+    atomicAdd(&st->wl_busy_ns, busy);
+    atomicAdd(&st->wl_wait_ns, t_end - t_begin - busy);
+    atomicMin(&st->wl_t0, t_begin);
+    atomicMax(&st->wl_t1, t_end);
   }
 }
 
@@ -1302,6 +1313,8 @@ __global__ void dawn_init_solve(KParams<V, EI> P) {
     st->R = st->W = st->FD = st->multi = 0ull;
     st->wl_head = st->wl_ctr = st->wl_items = 0ull;
     st->wl_mode = 0u;
+    st->wl_batches = st->wl_busy_ns = st->wl_wait_ns = st->wl_t1 = 0ull;
+    st->wl_t0 = ~0ull;
   }
 }
 

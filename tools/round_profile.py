@@ -86,6 +86,14 @@ def main():
         rate = x["edges"] / (x["x_us"] * 1e3) if x["x_us"] > 0 else 0
         print(f"{x['round']:>4} {x['entries']:>10} {x['edges']:>12} {x['s_us']:>8.1f} {x['x_us']:>9.1f} {rate:>8.1f}")
     print(f"sum S {tot_s:.1f} us, sum X {tot_x:.1f} us")
+    wl = (ctypes.c_uint64 * 6)()
+    N.check(L.dawn_solver_worklist_stats(s, wl, stream))
+    if wl[1]:
+        nwarps = max(1, (wl[3] + wl[4]) / max(wl[5], 1))
+        print(f"worklist: from round {wl[0]}, {wl[1]} items in {wl[2]} warp batches "
+              f"({wl[1] / max(wl[2], 1):.1f} items/batch), kernel span {wl[5] / 1e3:.1f} us, "
+              f"busy {wl[3] / 1e3 / nwarps:.1f} us per warp of {nwarps:.0f}, "
+              f"{wl[3] / max(wl[2], 1) / 1e3:.2f} us per batch")
     if rows and times:
         tail = min(times) * 1e3 - (buf[4 * rows[-1]["round"] + 2] - buf[4 * rows[0]["round"]]) / 1e3
         print(f"after the last recorded round (worklist kernel, if it ran, + launch gaps): {tail:.1f} us of the fastest solve")
