@@ -590,18 +590,24 @@ struct Impl {
     CK(cudaMalloc(&s->bst, sizeof(BState)));
     CK(cudaMemset(s->bst, 0, sizeof(BState)));
     CK(cudaMemset(s->bmask[0], 0, 4 * (size_t)n));
-    auto k = dawn_batch_persistent<V, EI>;
+    auto k = dawn_batch_persistent<V, EI, false>;
+    auto kl = dawn_batch_persistent<V, EI, true>;  // async schedule (live distance lines)
     const size_t sm = sizeof(BSmem<V, EI>);
     CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    CK(cudaFuncSetAttribute(kl, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     {
       const double need_kb = DAWN_BATCH_MIN_BLOCKS * ((double)(sm + 8 * 1024) / 1024.0 + 1.0);
       const int pct = std::min(100, (int)std::ceil(100.0 * need_kb / 228.0));
       CK(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+      CK(cudaFuncSetAttribute(kl, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
     }
     int bps = 0, nsm = 0, dev = 0;
     CK(cudaGetDevice(&dev));
     CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    int bpl = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k, NT, sm));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpl, kl, NT, sm));
+    bps = std::min(bps, bpl);  // one grid size for both instances
     if (bps < 1) return fail(DAWN_ECUDA, "batched kernel cannot be resident");
     const int64_t work = std::max<int64_t>((n + TILE - 1) / TILE, (m + BWT * WPB - 1) / (BWT * WPB));
     s->bgrid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)bps * nsm, work));
@@ -641,7 +647,7 @@ struct Impl {
   }
 
   // one batch of nl <= 32 sources; nmask is all-zero on entry and on exit
-  static int batch_run(dawn_solver_t s, const int64_t* src, int nl, int algo, cudaStream_t stream) {
+  static int batch_run(dawn_solver_t s, const int64_t* src, int nl, int algo, bool live, cudaStream_t stream) {
     TRY(batch_alloc(s));
     const int64_t n = s->g->n;
     CK(cudaMemsetAsync(s->bd, 0xFF, sizeof(K) * BL * (size_t)n, stream));
@@ -653,7 +659,8 @@ struct Impl {
     dawn_batch_init<V, EI><<<1, 32, 0, stream>>>(P);
     CK(cudaGetLastError());
     void* args[] = {&P};
-    CK(cudaLaunchCooperativeKernel((void*)dawn_batch_persistent<V, EI>, dim3(s->bgrid), dim3(NT), args, s->bsmem,
+    CK(cudaLaunchCooperativeKernel(live ? (void*)dawn_batch_persistent<V, EI, true> : (void*)dawn_batch_persistent<V, EI, false>,
+                                   dim3(s->bgrid), dim3(NT), args, s->bsmem,
                                    stream));
     return DAWN_OK;
   }
@@ -1052,7 +1059,7 @@ extern "C" int dawn_mssp_batch(dawn_solver_t s, const int64_t* sources, int64_t 
   s->last_batch = true;
   for (int64_t b = 0; b < nb; ++b) {
     const int nl = (int)std::min<int64_t>(BL, k - b * BL);
-    TRY(DISPATCH(s->g, batch_run(s, sources + b * BL, nl, algo, st)));
+    TRY(DISPATCH(s->g, batch_run(s, sources + b * BL, nl, algo, (flags & DAWN_F_ASYNC) != 0, st)));
     if (dist_out)
       TRY(DISPATCH(s->g, batch_decode(s, (char*)dist_out + (size_t)b * BL * ld * es, out_vtype, ld, nl, st)));
     if (stats_out) CK(cudaMemcpyAsync(s->bst_host + b, s->bst, sizeof(BState), cudaMemcpyDeviceToHost, st));

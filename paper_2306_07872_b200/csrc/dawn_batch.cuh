@@ -127,7 +127,7 @@ __device__ __forceinline__ T shfl_any(T v, int src) {
 // ---------------------------------------------------------------------------
 // B phase: consume nmask (round r-1's writes), build round r's frontier
 // ---------------------------------------------------------------------------
-template <class V, class EI>
+template <class V, class EI, bool LIVE>
 __device__ void bphase_build(const BParams<V, EI>& P, uint32_t r, uint32_t active, BSmem<V, EI>& s,
                              unsigned long long& accW, unsigned long long& accFD,
                              unsigned long long& accMW) {
@@ -289,8 +289,10 @@ __device__ void bphase_build(const BParams<V, EI>& P, uint32_t r, uint32_t activ
         const uint4* srcl = reinterpret_cast<const uint4*>(P.bd + (size_t)v * BL);
         uint4* dstl = reinterpret_cast<uint4*>(P.qkey + (size_t)pos * BL);
         uint4 x[8];
+        if (!LIVE) {
 #pragma unroll
-        for (int q = 0; q < 8; ++q) x[q] = __ldcg(srcl + q);
+          for (int q = 0; q < 8; ++q) x[q] = __ldcg(srcl + q);
+        }
         P.qnode[pos] = v;
         P.qmask[pos] = F[j];
         P.qoff[pos] = off;
@@ -300,14 +302,18 @@ __device__ void bphase_build(const BParams<V, EI>& P, uint32_t r, uint32_t activ
           const EI t1 = (off + dg - 1) / (EI)BWT;
           for (EI tt = t0; tt <= t1; ++tt) P.tile_row[tt] = pos;
         }
+        if (!LIVE) {  // the async schedule reads the live line instead
 #pragma unroll
-        for (int q = 0; q < 8; ++q) dstl[q] = x[q];
+          for (int q = 0; q < 8; ++q) dstl[q] = x[q];
+        }
+        if (!LIVE) {
 #pragma unroll
-        for (int h = 8; h < NV; h += 8) {  // 8-byte keys: second half of the line
+          for (int h = 8; h < NV; h += 8) {  // 8-byte keys: second half of the line
 #pragma unroll
-          for (int q = 0; q < 8; ++q) x[q] = __ldcg(srcl + h + q);
+            for (int q = 0; q < 8; ++q) x[q] = __ldcg(srcl + h + q);
 #pragma unroll
-          for (int q = 0; q < 8; ++q) dstl[h + q] = x[q];
+            for (int q = 0; q < 8; ++q) dstl[h + q] = x[q];
+          }
         }
         pos++;
         off += dg;
@@ -354,6 +360,7 @@ struct BTile {
   WB w;            // lane j: weight bits of edge j
   uint32_t kr;     // lane j: row of edge j, relative to i0
   uint32_t rmask;  // lane k: lane mask of row i0+k
+  uint32_t rnode;  // lane k: node of row i0+k (async schedule)
 };
 
 template <class V, class EI>
@@ -361,9 +368,10 @@ struct BRows {        // row metadata of a tile in flight
   uint32_t i0, il;
   EI off, base;       // lane k: row i0+k
   uint32_t rmask;
+  uint32_t rnode;
 };
 
-template <class V, class EI>
+template <class V, class EI, bool LIVE>
 __device__ __forceinline__ void brows_load(const BParams<V, EI>& P, EI t, EI T, uint32_t cnt, uint32_t lane,
                                            BRows<V, EI>& R) {
   R.i0 = __ldca(P.tile_row + t);
@@ -371,10 +379,12 @@ __device__ __forceinline__ void brows_load(const BParams<V, EI>& P, EI t, EI T, 
   R.off = 0;
   R.base = 0;
   R.rmask = 0;
+  R.rnode = 0;
   if (lane <= R.il - R.i0) {
     R.off = __ldca(P.qoff + R.i0 + lane);
     R.base = __ldca(P.qbase + R.i0 + lane);
     R.rmask = __ldca(P.qmask + R.i0 + lane);
+    if (LIVE) R.rnode = __ldca(P.qnode + R.i0 + lane);
   }
 }
 
@@ -386,6 +396,7 @@ __device__ __forceinline__ void btile_issue(const BParams<V, EI>& P, EI t, EI E,
   X.len = (E - e0 < (EI)BWT) ? (uint32_t)(E - e0) : (uint32_t)BWT;
   X.i0 = R.i0;
   X.rmask = R.rmask;
+  X.rnode = R.rnode;
   const uint32_t nrows = R.il - R.i0 + 1;
   const uint32_t rst = (lane < nrows && R.off >= e0 && R.off - e0 < (EI)32) ? (uint32_t)(R.off - e0) : 32u;
   const uint32_t B = __reduce_or_sync(0xffffffffu, rst < 32u ? (1u << rst) : 0u);
@@ -401,7 +412,7 @@ __device__ __forceinline__ void btile_issue(const BParams<V, EI>& P, EI t, EI E,
 // first rounds, where every source still explores its own neighbourhood): a
 // thread owns one edge and walks the row's set lanes one by one (scalar
 // gathers), instead of 8 threads covering all 32 lanes of the distance line.
-template <class V, class EI, bool SPARSE>
+template <class V, class EI, bool SPARSE, bool LIVE>
 __device__ void bphase_expand(const BParams<V, EI>& P, uint32_t r, const uint32_t (&msrc)[BLanes<V>::LPT],
                               unsigned& guard, unsigned& wrote, unsigned long long (&accR)[BLanes<V>::LPT],
                               BSmem<V, EI>& sm) {
@@ -437,17 +448,17 @@ __device__ void bphase_expand(const BParams<V, EI>& P, uint32_t r, const uint32_
   BRows<V, EI> Rn;
   {
     BRows<V, EI> R0;
-    brows_load<V, EI>(P, t, T, cnt, lane, R0);
+    brows_load<V, EI, LIVE>(P, t, T, cnt, lane, R0);
     btile_issue<V, EI>(P, t, E, lane, R0, A);
   }
   Bt.len = 0;
   if (t + GW < T) {
     BRows<V, EI> R1;
-    brows_load<V, EI>(P, t + GW, T, cnt, lane, R1);
+    brows_load<V, EI, LIVE>(P, t + GW, T, cnt, lane, R1);
     btile_issue<V, EI>(P, t + GW, E, lane, R1, Bt);
   }
   bool have_rn = t + 2 * GW < T;
-  if (have_rn) brows_load<V, EI>(P, t + 2 * GW, T, cnt, lane, Rn);
+  if (have_rn) brows_load<V, EI, LIVE>(P, t + 2 * GW, T, cnt, lane, Rn);
   // relaxations (solver.py:297, :372) of this thread's lanes: LPT 8/16-bit
   // counters packed in one register (a thread sees STEPS <= 16 edges per tile),
   // flushed into accR after every tile
@@ -459,12 +470,14 @@ __device__ void bphase_expand(const BParams<V, EI>& P, uint32_t r, const uint32_
       // ---- relax tile A, lane-sparse: lane j = edge j, loop over the row's lanes ----
       const uint32_t mrow = __shfl_sync(0xffffffffu, A.rmask, A.kr & 31);
       uint32_t lanes = lane < A.len ? mrow : 0u;
-      const size_t rowk = (size_t)(A.i0 + A.kr) * BL;
+      // the row's line: its round-start snapshot, or (async) the live line bd[u]
+      const uint32_t rnode = LIVE ? __shfl_sync(0xffffffffu, A.rnode, A.kr & 31) : 0u;
+      const K* rowl = LIVE ? P.bd + (size_t)rnode * BL : P.qkey + (size_t)(A.i0 + A.kr) * BL;
       while (lanes) {
         const uint32_t l = __ffs(lanes) - 1;
         lanes &= lanes - 1u;
         atomicAdd(&sm.rl[l], 1u);  // relaxation of source lane l (solver.py:297, :372)
-        const K c = CD::relax(CD::dec(__ldca(P.qkey + rowk + l)), A.w);
+        const K c = CD::relax(CD::dec(__ldca(rowl + l)), A.w);
         const K cur = __ldca(P.bd + (size_t)A.col * BL + l);
         if (c < CAP && c < cur) {
           if (A.col == sm.src[l]) {
@@ -495,10 +508,11 @@ __device__ void bphase_expand(const BParams<V, EI>& P, uint32_t r, const uint32_
         const uint32_t kq = __shfl_sync(0xffffffffu, A.kr, j & 31);
         const WB wq = shfl_any<WB>(A.w, j & 31);
         const uint32_t mq = __shfl_sync(0xffffffffu, A.rmask, kq & 31);
+        const uint32_t nq = LIVE ? __shfl_sync(0xffffffffu, A.rnode, kq & 31) : 0u;
         const uint32_t a = (j < A.len) ? ((mq >> lsh) & LMASK) : 0u;
-        if (kq != ck) {  // the row's snapshot (L1)
+        if (kq != ck) {  // the row's snapshot, or (async) its live line (L1)
           ck = kq;
-          ld16_ca<K, LPT>(P.qkey + (size_t)(A.i0 + kq) * BL + lsh, cs);
+          ld16_ca<K, LPT>((LIVE ? P.bd + (size_t)nq * BL : P.qkey + (size_t)(A.i0 + kq) * BL) + lsh, cs);
         }
 #pragma unroll
         for (int i = 0; i < LPT; ++i) cand[u][i] = CD::relax(CD::dec(cs[i]), wq);
@@ -543,7 +557,7 @@ __device__ void bphase_expand(const BParams<V, EI>& P, uint32_t r, const uint32_
     if (have_rn) {
       btile_issue<V, EI>(P, t + GW, E, lane, Rn, Bt);
       have_rn = t + 2 * GW < T;
-      if (have_rn) brows_load<V, EI>(P, t + 2 * GW, T, cnt, lane, Rn);
+      if (have_rn) brows_load<V, EI, LIVE>(P, t + 2 * GW, T, cnt, lane, Rn);
     }
   }
 }
@@ -551,7 +565,7 @@ __device__ void bphase_expand(const BParams<V, EI>& P, uint32_t r, const uint32_
 // ---------------------------------------------------------------------------
 // the persistent batched kernel
 // ---------------------------------------------------------------------------
-template <class V, class EI>
+template <class V, class EI, bool LIVE>
 __global__ void __launch_bounds__(NT, DAWN_BATCH_MIN_BLOCKS) dawn_batch_persistent(BParams<V, EI> P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   BSmem<V, EI>& s = *reinterpret_cast<BSmem<V, EI>*>(smem_raw);
@@ -595,7 +609,7 @@ __global__ void __launch_bounds__(NT, DAWN_BATCH_MIN_BLOCKS) dawn_batch_persiste
       st->res[(r + 1) & 1] = 0ull;
       st->le[(r + 1) & 1] = 0ull;
     }
-    bphase_build<V, EI>(P, r, active, s, accW, accFD, accMW);
+    bphase_build<V, EI, LIVE>(P, r, active, s, accW, accFD, accMW);
     grid_sync(&st->bar);
     // ---- X phase ----
     if (prof) {
@@ -608,8 +622,8 @@ __global__ void __launch_bounds__(NT, DAWN_BATCH_MIN_BLOCKS) dawn_batch_persiste
       // lane-sparse relax when the round's rows carry few active sources on average
       const unsigned long long E = pk_edges(ldcg(&st->res[r & 1]), P.ebits);
       const unsigned long long LE = ldcg(&st->le[r & 1]);
-      if (LE < (unsigned long long)P.sparse_util * E) bphase_expand<V, EI, true>(P, r, msrc, guard, wrote, accR, s);
-      else bphase_expand<V, EI, false>(P, r, msrc, guard, wrote, accR, s);
+      if (LE < (unsigned long long)P.sparse_util * E) bphase_expand<V, EI, true, LIVE>(P, r, msrc, guard, wrote, accR, s);
+      else bphase_expand<V, EI, false, LIVE>(P, r, msrc, guard, wrote, accR, s);
     }
     wrote = __reduce_or_sync(0xffffffffu, wrote);
     if (lane == 0 && wrote) atomicOr(&st->wrote[r & 1], wrote);

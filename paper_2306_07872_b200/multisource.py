@@ -55,16 +55,22 @@ def _stats_list(arr, k):
 
 
 def mssp_tile(g, sources: Sequence[int], algo: str = "govm", *, precision: str | None = None,
-              out=None, out_dtype=None, stats: bool = True, device: int | None = None):
+              out=None, out_dtype=None, stats: bool = True, device: int | None = None,
+              schedule: str | None = None):
     """Distances from every source into a device tensor tile ``[k][n]``.
 
     ``out``: optional preallocated CUDA tensor view ``[k][ld >= n]`` (row
     stride ``ld``) of dtype ``out_dtype``; float64 by default, float32
     allowed for float32 graphs.  Returns ``(tile, stats)`` with ``stats`` a
     list of :class:`SolveStats` (or None when ``stats=False``, in which case
-    the call is asynchronous on the current stream).
+    the call is asynchronous on the current stream).  ``schedule``:
+    ``jacobi`` / ``async`` as in :func:`gsvm_sssp`.
     """
     import torch
+
+    from .solver import _schedule_flag
+
+    sflag = _schedule_flag(schedule)
 
     dg = device_graph(g, device=device, precision=precision)
     src = np.ascontiguousarray([int(s) for s in sources], dtype=np.int64)
@@ -93,12 +99,12 @@ def mssp_tile(g, sources: Sequence[int], algo: str = "govm", *, precision: str |
         sup = ctypes.c_int(0)
         N.check(N.lib().dawn_batch_supported(s, algo_id, 0, ctypes.byref(sup)))
         if sup.value:
-            N.check(N.lib().dawn_mssp_batch(s, src.ctypes.data, k, algo_id, 0, out.data_ptr(), vt, ld,
+            N.check(N.lib().dawn_mssp_batch(s, src.ctypes.data, k, algo_id, sflag, out.data_ptr(), vt, ld,
                                             ctypes.addressof(st_arr) if stats else None, stream))
         else:
             # negative weights: one persistent solve per source (integer graphs keep the
             # early negative-cycle exit), float64 rows
-            flags = N.F_NEGCHECK if dg.vtype in (N.I32, N.I64) else 0
+            flags = (N.F_NEGCHECK if dg.vtype in (N.I32, N.I64) else 0) | sflag
             s2 = dg.solver(flags)
             row = out if vt == N.F64 else torch.empty((k, n), dtype=torch.float64, device=dev)
             for i in range(k):
@@ -144,7 +150,8 @@ def _p2p_possible(root_dev: int, my_dev: int) -> bool:
 
 def apsp_sharded(g, sources: Sequence[int], algo: str = "govm", *, precision: str | None = None,
                  group=None, root: int = 0, out_dtype=None, transport: str = "auto",
-                 solve_fn: Callable | None = None, tile=None, ring: int = 3) -> ShardedResult:
+                 solve_fn: Callable | None = None, tile=None, ring: int = 3,
+                 schedule: str | None = None) -> ShardedResult:
     """Multi-source solve sharded over the ranks of ``group`` (one process per GPU).
 
     Every rank must call it with the same ``g`` (replicated) and ``sources``.
@@ -196,7 +203,7 @@ def apsp_sharded(g, sources: Sequence[int], algo: str = "govm", *, precision: st
             rows, st = solve_fn(lo, hi)
             out_rows.copy_(rows)
             return st
-        _, st = mssp_tile(dg, src[lo:hi], algo, out=out_rows, out_dtype=out_dtype, stats=True)
+        _, st = mssp_tile(dg, src[lo:hi], algo, out=out_rows, out_dtype=out_dtype, stats=True, schedule=schedule)
         return st
 
     stats_local: list[tuple[int, list]] = []

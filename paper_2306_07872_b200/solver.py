@@ -380,9 +380,10 @@ SOLVERS = {"gsvm": gsvm_sssp, "govm": govm_sssp}
 _ROW_BYTES_BUDGET = 1 << 30  # float64 rows copied back per dawn_mssp call
 
 
-def _mssp_on_device(g, sources: list[int], algo: int, device: int, precision: str | None):
+def _mssp_on_device(g, sources: list[int], algo: int, device: int, precision: str | None,
+                    schedule: str | None = None):
     dg = device_graph(g, device=device, precision=precision)
-    flags = _neg_flags(dg)
+    flags = _neg_flags(dg) | _schedule_flag(schedule)
     n = dg.n
     rows = np.empty((len(sources), n), dtype=np.float64)
     stats = (N.Stats * max(len(sources), 1))()
@@ -406,12 +407,15 @@ def _devices_for(workers: int) -> list[int]:
 
 
 def mssp(g, sources: Sequence[int], algo: str = "govm", workers: int = 1, *,
-         precision: str | None = None) -> list[tuple[DistanceVector, SolveStats]]:
+         precision: str | None = None, schedule: str | None = None) -> list[tuple[DistanceVector, SolveStats]]:
     """Independent solves from each source, results in the given order (solver.py:426-457).
 
     ``workers`` is the number of GPUs the sources are spread over (capped at
     the visible device count); results are bit-identical for any value.
+    ``schedule`` as in :func:`gsvm_sssp` (``async``: same rows, per-source
+    counters timing-dependent).
     """
+    _schedule_flag(schedule)  # validate before any work
     name = _normalize_algo(algo)
     if workers < 1:
         raise ValueError("workers must be >= 1")
@@ -423,11 +427,11 @@ def mssp(g, sources: Sequence[int], algo: str = "govm", workers: int = 1, *,
     algo_id = _ALGO[name]
     devs = _devices_for(workers)
     if len(devs) == 1 or len(sources) == 1:
-        return _mssp_on_device(g, sources, algo_id, devs[0], precision)
+        return _mssp_on_device(g, sources, algo_id, devs[0], precision, schedule)
     # contiguous blocks, one host thread per GPU; order restored by block index
     blocks = np.array_split(np.arange(len(sources)), len(devs))
     with ThreadPoolExecutor(max_workers=len(devs)) as ex:
-        futs = [ex.submit(_mssp_on_device, g, [sources[i] for i in blk], algo_id, d, precision)
+        futs = [ex.submit(_mssp_on_device, g, [sources[i] for i in blk], algo_id, d, precision, schedule)
                 for d, blk in zip(devs, blocks) if len(blk)]
         out = []
         for f in futs:
@@ -436,7 +440,7 @@ def mssp(g, sources: Sequence[int], algo: str = "govm", workers: int = 1, *,
 
 
 def apsp(g, algo: str = "govm", workers: int = 1, sink: Callable[[DistanceVector], None] | None = None, *,
-         precision: str | None = None) -> AggregateStats:
+         precision: str | None = None, schedule: str | None = None) -> AggregateStats:
     """Every source in ascending order, rows streamed to ``sink`` (solver.py:460-495).
 
     Rows are produced in device batches and handed to ``sink`` strictly in
@@ -449,6 +453,7 @@ def apsp(g, algo: str = "govm", workers: int = 1, sink: Callable[[DistanceVector
     name = _normalize_algo(algo)
     if workers < 1:
         raise ValueError("workers must be >= 1")
+    _schedule_flag(schedule)
     agg = AggregateStats()
     n = g.n
     if n == 0:
@@ -456,15 +461,17 @@ def apsp(g, algo: str = "govm", workers: int = 1, sink: Callable[[DistanceVector
     batch = max(1, min(n, (256 << 20) // (8 * n)))
     if workers > 1 and N.device_count() > 1:
         for lo in range(0, n, batch):
-            for dv, st in mssp(g, range(lo, min(n, lo + batch)), name, workers, precision=precision):
+            for dv, st in mssp(g, range(lo, min(n, lo + batch)), name, workers, precision=precision,
+                               schedule=schedule):
                 if sink is not None:
                     sink(dv)
                 agg.add(st)
         return agg.finish()
-    return _apsp_pipelined(g, name, sink, precision, batch, agg)
+    return _apsp_pipelined(g, name, sink, precision, batch, agg, schedule)
 
 
-def _apsp_pipelined(g, name: str, sink, precision, batch: int, agg: AggregateStats) -> AggregateStats:
+def _apsp_pipelined(g, name: str, sink, precision, batch: int, agg: AggregateStats,
+                    schedule: str | None = None) -> AggregateStats:
     import queue
 
     import torch
@@ -472,7 +479,7 @@ def _apsp_pipelined(g, name: str, sink, precision, batch: int, agg: AggregateSta
     dg = device_graph(g, precision=precision)
     n = dg.n
     algo_id = _ALGO[name]
-    flags = _neg_flags(dg)
+    flags = _neg_flags(dg) | _schedule_flag(schedule)
     bufs = [torch.empty((batch, n), dtype=torch.float64).pin_memory() for _ in range(2)]
     free: "queue.Queue[int]" = queue.Queue()
     for i in range(2):

@@ -132,3 +132,44 @@ def test_edgeless_and_isolated(gpu):
     g = make_csr(3, [(1, 2, 1.0)])
     tile, stats = MS.mssp_tile(g, [0, 1, 0, 1], "gsvm")
     check_rows(g, [0, 1, 0, 1], "gsvm", tile, stats)
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_batch_async_rows(gpu, seed, lane_mode):
+    """Async batches (live distance lines instead of round-start snapshots):
+    every row and first_discoveries equal the Jacobi batch / oracle."""
+    rng = np.random.default_rng(300 + seed)
+    n = int(rng.integers(2, 900))
+    m = int(rng.integers(0, 10 * n))
+    u, v = rng.integers(0, n, m), rng.integers(0, n, m)
+    w = rng.integers(0, 40, m).astype(float) if seed % 2 == 0 else rng.uniform(0, 2, m)
+    g = P.csr_from_arrays(n, u, v, w)
+    k = [1, 5, 32, 33, 70, 64, 40, 2][seed]
+    src = [int(x) for x in rng.integers(0, n, k)]
+    for algo in ("govm", "gsvm"):
+        tj, sj = MS.mssp_tile(g, src, algo, schedule="jacobi")
+        ta, sa = MS.mssp_tile(g, src, algo, schedule="async")
+        assert same(ta.cpu().numpy(), tj.cpu().numpy()), algo
+        for a, b in zip(sa, sj):
+            assert a.first_discoveries == b.first_discoveries and a.negative_cycle == b.negative_cycle
+            assert a.writes >= a.first_discoveries
+
+
+def test_batch_async_rmat_and_api(gpu):
+    g = G.rmat_graph(15, 16, weights="f32")
+    src = list(range(0, 3000, 37))
+    tj, sj = MS.mssp_tile(g, src, "govm", precision="fp32", out_dtype=torch.float32, schedule="jacobi")
+    ta, sa = MS.mssp_tile(g, src, "govm", precision="fp32", out_dtype=torch.float32, schedule="async")
+    assert torch.equal(ta, tj)
+    assert sum(s.relaxations for s in sa) <= sum(s.relaxations for s in sj)
+    gi = G.rmat_graph(12, 8, weights="int")
+    rows = P.mssp(gi, range(0, 200, 3), "govm", schedule="async")
+    for s, (dv, st) in zip(range(0, 200, 3), rows):
+        assert same(dv.dist, O.gs_sssp(gi, s)[0])
+    got = []
+    agg = P.apsp(gi, "govm", sink=got.append, schedule="async")
+    assert [d.source for d in got] == list(range(gi.n))
+    assert same(got[77].dist, O.gs_sssp(gi, 77)[0])
+    assert agg is not None
+    with pytest.raises(ValueError):
+        P.mssp(gi, [0], schedule="chaotic")
