@@ -1,7 +1,7 @@
 // dawn.cu — C ABI (include/dawn.h) over the sm_100a weighted-DAWN kernels.
 //
 // Memory model: the graph and each solver's workspace are allocated once
-// (cudaMalloc, outside any solve); a solve performs no allocation.  Device
+// (from the device memory pool, outside any solve); a solve performs no allocation.  Device
 // layout per graph (32-bit indices when m < 2^32):
 //   row_ptr : EI[n+1]
 //   edges   : uint2 {col, weight bits}[m]        (4-byte value types: 8 B/edge, one LDG.64)
@@ -18,7 +18,10 @@
 #include <algorithm>
 #include <type_traits>
 #include <climits>
+#include <mutex>
 #include <string>
+#include <utility>
+#include <vector>
 
 #include "../../include/dawn.h"
 #include "dawn_batch.cuh"
@@ -55,6 +58,77 @@ static int fail(int code, const char* fmt, ...) {
     int rc_ = (expr);          \
     if (rc_ != DAWN_OK) return rc_; \
   } while (0)
+
+// ---------------------------------------------------------------------------
+// memory: device buffers come from the device's stream-ordered pool with an
+// unbounded release threshold, so creating and destroying graphs / solvers of
+// the same sizes (a plugin handle per call, the e2e bench step) reuses memory
+// instead of paying cudaMalloc + cudaFree (~16 ms for a config-2 solver).
+// Frees follow a device synchronisation, as cudaFree's implicit one did.
+// Small pinned host blocks (state read-back) are cached the same way.
+// ---------------------------------------------------------------------------
+static std::mutex g_mem_mu;
+static bool g_pool_ready[128];
+
+static cudaError_t dmalloc_raw(void** p, size_t bytes) {
+  *p = nullptr;
+  if (bytes == 0) return cudaSuccess;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  {
+    std::lock_guard<std::mutex> lk(g_mem_mu);
+    if (dev >= 0 && dev < 128 && !g_pool_ready[dev]) {
+      cudaMemPool_t pool;
+      if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+      }
+      g_pool_ready[dev] = true;
+    }
+  }
+  e = cudaMallocAsync(p, bytes, 0);
+  if (e != cudaSuccess) {
+    *p = nullptr;
+    return e;
+  }
+  return cudaStreamSynchronize(0);  // usable from any stream from here on
+}
+template <class T>
+static cudaError_t dmalloc(T** p, size_t bytes) {
+  return dmalloc_raw(reinterpret_cast<void**>(p), bytes);
+}
+static void dfree(void* p) {
+  if (p) cudaFreeAsync(p, 0);
+}
+
+static std::vector<std::pair<size_t, void*>> g_host_free;  // cached pinned blocks (size, ptr)
+template <class T>
+static cudaError_t hmalloc(T** p, size_t bytes) {
+  {
+    std::lock_guard<std::mutex> lk(g_mem_mu);
+    for (size_t i = 0; i < g_host_free.size(); ++i) {
+      if (g_host_free[i].first == bytes) {
+        *p = reinterpret_cast<T*>(g_host_free[i].second);
+        g_host_free.erase(g_host_free.begin() + (long)i);
+        return cudaSuccess;
+      }
+    }
+  }
+  void* q = nullptr;
+  cudaError_t e = cudaMallocHost(&q, bytes + 16);  // + 16: the block remembers its size
+  if (e != cudaSuccess) return e;
+  *reinterpret_cast<size_t*>(q) = bytes;
+  *p = reinterpret_cast<T*>(reinterpret_cast<char*>(q) + 16);
+  return cudaSuccess;
+}
+static void hfree(void* p) {
+  if (!p) return;
+  char* q = reinterpret_cast<char*>(p) - 16;
+  std::lock_guard<std::mutex> lk(g_mem_mu);
+  if (g_host_free.size() < 64) g_host_free.emplace_back(*reinterpret_cast<size_t*>(q), p);
+  else cudaFreeHost(q);
+}
 
 // ---------------------------------------------------------------------------
 // objects
@@ -282,10 +356,11 @@ static int convert_graph(dawn_graph_t g, const int64_t* d_rp, const int64_t* d_c
 static void graph_free(dawn_graph_t g) {
   if (!g) return;
   cudaSetDevice(g->device);
-  cudaFree(g->row_ptr);
-  cudaFree(g->e2);
-  cudaFree(g->ecol);
-  cudaFree(g->ew);
+  cudaDeviceSynchronize();
+  dfree(g->row_ptr);
+  dfree(g->e2);
+  dfree(g->ecol);
+  dfree(g->ew);
   delete g;
 }
 
@@ -316,17 +391,17 @@ extern "C" int dawn_graph_create(int device, int64_t n, int64_t m, const int64_t
   const size_t eis = g->wide ? 8 : 4;
   auto cleanup = [&](int rc) { graph_free(g); return rc; };
   cudaError_t e;
-  if ((e = cudaMalloc(&g->row_ptr, eis * (size_t)(n + 1))) != cudaSuccess)
+  if ((e = dmalloc(&g->row_ptr, eis * (size_t)(n + 1))) != cudaSuccess)
     return cleanup(fail(DAWN_ENOMEM, "row_ptr alloc: %s", cudaGetErrorString(e)));
   g->bytes += eis * (n + 1);
   const size_t mm = (size_t)std::max<int64_t>(m, 1);
   if (value_size(vtype) == 4) {
-    if ((e = cudaMalloc(&g->e2, 8 * mm)) != cudaSuccess)
+    if ((e = dmalloc(&g->e2, 8 * mm)) != cudaSuccess)
       return cleanup(fail(DAWN_ENOMEM, "edge alloc: %s", cudaGetErrorString(e)));
     g->bytes += 8 * mm;
   } else {
-    if ((e = cudaMalloc(&g->ecol, 4 * mm)) != cudaSuccess ||
-        (e = cudaMalloc(&g->ew, 8 * mm)) != cudaSuccess)
+    if ((e = dmalloc(&g->ecol, 4 * mm)) != cudaSuccess ||
+        (e = dmalloc(&g->ew, 8 * mm)) != cudaSuccess)
       return cleanup(fail(DAWN_ENOMEM, "edge alloc: %s", cudaGetErrorString(e)));
     g->bytes += 12 * mm;
   }
@@ -351,7 +426,7 @@ extern "C" int dawn_graph_create(int device, int64_t n, int64_t m, const int64_t
     }
   } else if (!src_is_device) {
     const size_t bytes = 8 * (size_t)(n + 1) + 16 * (size_t)m;
-    if ((e = cudaMalloc(&tmp, bytes)) != cudaSuccess)
+    if ((e = dmalloc(&tmp, bytes)) != cudaSuccess)
       return cleanup(fail(DAWN_ENOMEM, "staging alloc: %s", cudaGetErrorString(e)));
     char* p = (char*)tmp;
     int64_t* s_rp = (int64_t*)p;
@@ -361,16 +436,16 @@ extern "C" int dawn_graph_create(int device, int64_t n, int64_t m, const int64_t
     if (e == cudaSuccess && m) e = cudaMemcpy(s_col, col, 8 * (size_t)m, cudaMemcpyHostToDevice);
     if (e == cudaSuccess && m) e = cudaMemcpy(s_val, val, 8 * (size_t)m, cudaMemcpyHostToDevice);
     if (e != cudaSuccess) {
-      cudaFree(tmp);
+      dfree(tmp);
       return cleanup(fail(DAWN_ECUDA, "graph upload: %s", cudaGetErrorString(e)));
     }
     d_rp = s_rp;
     d_col = s_col;
     d_val = s_val;
   }
-  if ((e = cudaMalloc(&d_flags, sizeof(unsigned))) != cudaSuccess ||
+  if ((e = dmalloc(&d_flags, sizeof(unsigned))) != cudaSuccess ||
       (e = cudaMemset(d_flags, 0, sizeof(unsigned))) != cudaSuccess) {
-    cudaFree(tmp);
+    dfree(tmp);
     return cleanup(fail(DAWN_ECUDA, "flags: %s", cudaGetErrorString(e)));
   }
   int rc = DAWN_OK;
@@ -385,8 +460,8 @@ extern "C" int dawn_graph_create(int device, int64_t n, int64_t m, const int64_t
     e = cudaMemcpy(&hflags, d_flags, sizeof(unsigned), cudaMemcpyDeviceToHost);
     if (e != cudaSuccess) rc = fail(DAWN_ECUDA, "graph convert: %s", cudaGetErrorString(e));
   }
-  cudaFree(tmp);
-  cudaFree(d_flags);
+  dfree(tmp);
+  dfree(d_flags);
   if (rc != DAWN_OK) return cleanup(rc);
   if (hflags & ERR_ROWPTR) return cleanup(fail(DAWN_EINVAL, "row_ptr must start at 0, end at m and be monotone"));
   if (hflags & ERR_COL) return cleanup(fail(DAWN_EINVAL, "column index out of range"));
@@ -579,15 +654,15 @@ struct Impl {
     if (s->batch_ready) return DAWN_OK;
     const int64_t n = s->g->n, m = s->g->m;
     const size_t ks = sizeof(K), es = sizeof(EI);
-    CK(cudaMalloc(&s->bd, ks * BL * (size_t)n));
-    for (int i = 0; i < 4; ++i) CK(cudaMalloc(&s->bmask[i], 4 * (size_t)n));
-    CK(cudaMalloc(&s->bqnode, 4 * (size_t)n));
-    CK(cudaMalloc(&s->bqmask, 4 * (size_t)n));
-    CK(cudaMalloc(&s->bqoff, es * (size_t)n));
-    CK(cudaMalloc(&s->bqbase, es * (size_t)n));
-    CK(cudaMalloc(&s->bqkey, ks * BL * (size_t)n));
-    CK(cudaMalloc(&s->btile, 4 * (size_t)(m / BWT + 4)));
-    CK(cudaMalloc(&s->bst, sizeof(BState)));
+    CK(dmalloc(&s->bd, ks * BL * (size_t)n));
+    for (int i = 0; i < 4; ++i) CK(dmalloc(&s->bmask[i], 4 * (size_t)n));
+    CK(dmalloc(&s->bqnode, 4 * (size_t)n));
+    CK(dmalloc(&s->bqmask, 4 * (size_t)n));
+    CK(dmalloc(&s->bqoff, es * (size_t)n));
+    CK(dmalloc(&s->bqbase, es * (size_t)n));
+    CK(dmalloc(&s->bqkey, ks * BL * (size_t)n));
+    CK(dmalloc(&s->btile, 4 * (size_t)(m / BWT + 4)));
+    CK(dmalloc(&s->bst, sizeof(BState)));
     CK(cudaMemset(s->bst, 0, sizeof(BState)));
     CK(cudaMemset(s->bmask[0], 0, 4 * (size_t)n));
     auto k = dawn_batch_persistent<V, EI, false>;
@@ -673,7 +748,7 @@ struct Impl {
     const size_t es = out_vt == DAWN_F64 ? 8 : 4;
     void* target = out;
     if (!dev) {
-      if (!s->bout) CK(cudaMalloc(&s->bout, 8 * BL * (size_t)n));
+      if (!s->bout) CK(dmalloc(&s->bout, 8 * BL * (size_t)n));
       target = s->bout;
     }
     const int64_t tld = dev ? ld : n;
@@ -693,10 +768,10 @@ struct Impl {
   static int alloc(dawn_solver_t s) {
     const int64_t n = s->g->n, m = s->g->m;
     const size_t ks = sizeof(K), es = sizeof(EI);
-    CK(cudaMalloc(&s->dist, ks * n));
-    CK(cudaMalloc(&s->stamp, 4 * n));
-    CK(cudaMalloc(&s->bmap, 4 * (size_t)((n + 31) / 32 + 4)));  // padded for 16-byte loads
-    CK(cudaMalloc(&s->wstate, (size_t)n + 4));  // + 4: the worklist tail updates it by 32-bit words
+    CK(dmalloc(&s->dist, ks * n));
+    CK(dmalloc(&s->stamp, 4 * n));
+    CK(dmalloc(&s->bmap, 4 * (size_t)((n + 31) / 32 + 4)));  // padded for 16-byte loads
+    CK(dmalloc(&s->wstate, (size_t)n + 4));  // + 4: the worklist tail updates it by 32-bit words
     if (!s->g->has_negative) {
       // worklist tail (async schedule): ring of items (every node once + long-row chunks + slack;
       // a full ring only makes producers wait)
@@ -704,30 +779,30 @@ struct Impl {
       uint64_t cap = 1;
       while (cap < need) cap <<= 1;
       s->wl_cap = cap;
-      CK(cudaMalloc(&s->wl_ring, 16 * cap));  // 16-byte items; node field 0xFFFFFFFF = empty
+      CK(dmalloc(&s->wl_ring, 16 * cap));  // 16-byte items; node field 0xFFFFFFFF = empty
       CK(cudaMemset(s->wl_ring, 0xFF, 16 * cap));
     }
     if (s->flags & (DAWN_F_PRED | DAWN_F_NEGCHECK)) {
-      CK(cudaMalloc(&s->pred, 8 * n));
-      CK(cudaMalloc(&s->jmp0, 4 * n));
-      CK(cudaMalloc(&s->jmp1, 4 * n));
-      CK(cudaMalloc(&s->pbuf, 8 * n));
+      CK(dmalloc(&s->pred, 8 * n));
+      CK(dmalloc(&s->jmp0, 4 * n));
+      CK(dmalloc(&s->jmp1, 4 * n));
+      CK(dmalloc(&s->pbuf, 8 * n));
     }
     for (int i = 0; i < 2; ++i) {
-      CK(cudaMalloc(&s->qnode[i], 4 * n));
-      CK(cudaMalloc(&s->qoff[i], es * n));
-      CK(cudaMalloc(&s->qbase[i], es * n));
-      CK(cudaMalloc(&s->qkey[i], ks * n));
+      CK(dmalloc(&s->qnode[i], 4 * n));
+      CK(dmalloc(&s->qoff[i], es * n));
+      CK(dmalloc(&s->qbase[i], es * n));
+      CK(dmalloc(&s->qkey[i], ks * n));
     }
-    CK(cudaMalloc(&s->tile_row, 4 * (size_t)(m / WT_MIN + 4)));
-    CK(cudaMalloc(&s->st, sizeof(DevState)));
+    CK(dmalloc(&s->tile_row, 4 * (size_t)(m / WT_MIN + 4)));
+    CK(dmalloc(&s->st, sizeof(DevState)));
     CK(cudaMemset(s->st, 0, sizeof(DevState)));
-    CK(cudaMallocHost(&s->st_host, sizeof(DevState)));
-    CK(cudaMalloc(&s->dbuf, 8 * n));
+    CK(hmalloc(&s->st_host, sizeof(DevState)));
+    CK(dmalloc(&s->dbuf, 8 * n));
     if (s->flags & DAWN_F_PROFILE) {
       s->prof_cap = 1u << 16;
-      CK(cudaMalloc(&s->prof, 32 * (size_t)s->prof_cap));
-      CK(cudaMalloc(&s->cta_prof, 8 * 2 * 2048 * (size_t)CTA_PROF_ROUNDS));
+      CK(dmalloc(&s->prof, 32 * (size_t)s->prof_cap));
+      CK(dmalloc(&s->cta_prof, 8 * 2 * 2048 * (size_t)CTA_PROF_ROUNDS));
       CK(cudaMemset(s->cta_prof, 0, 8 * 2 * 2048 * (size_t)CTA_PROF_ROUNDS));
     }
     return setup(s);
@@ -751,38 +826,39 @@ struct Impl {
 static void solver_free(dawn_solver_t s) {
   if (!s) return;
   cudaSetDevice(s->g->device);
-  cudaFree(s->dist);
-  cudaFree(s->stamp);
-  cudaFree(s->bmap);
-  cudaFree(s->wstate);
-  cudaFree(s->pred);
-  cudaFree(s->jmp0);
-  cudaFree(s->jmp1);
-  cudaFree(s->pbuf);
+  cudaDeviceSynchronize();
+  dfree(s->dist);
+  dfree(s->stamp);
+  dfree(s->bmap);
+  dfree(s->wstate);
+  dfree(s->pred);
+  dfree(s->jmp0);
+  dfree(s->jmp1);
+  dfree(s->pbuf);
   for (int i = 0; i < 2; ++i) {
-    cudaFree(s->qnode[i]);
-    cudaFree(s->qoff[i]);
-    cudaFree(s->qbase[i]);
-    cudaFree(s->qkey[i]);
+    dfree(s->qnode[i]);
+    dfree(s->qoff[i]);
+    dfree(s->qbase[i]);
+    dfree(s->qkey[i]);
   }
-  cudaFree(s->tile_row);
-  cudaFree(s->wl_ring);
-  cudaFree(s->st);
-  cudaFreeHost(s->st_host);
-  cudaFree(s->dbuf);
-  cudaFree(s->prof);
-  cudaFree(s->cta_prof);
-  cudaFree(s->bd);
-  for (int i = 0; i < 4; ++i) cudaFree(s->bmask[i]);
-  cudaFree(s->bqnode);
-  cudaFree(s->bqmask);
-  cudaFree(s->bqoff);
-  cudaFree(s->bqbase);
-  cudaFree(s->bqkey);
-  cudaFree(s->btile);
-  cudaFree(s->bst);
-  cudaFreeHost(s->bst_host);
-  cudaFree(s->bout);
+  dfree(s->tile_row);
+  dfree(s->wl_ring);
+  dfree(s->st);
+  hfree(s->st_host);
+  dfree(s->dbuf);
+  dfree(s->prof);
+  dfree(s->cta_prof);
+  dfree(s->bd);
+  for (int i = 0; i < 4; ++i) dfree(s->bmask[i]);
+  dfree(s->bqnode);
+  dfree(s->bqmask);
+  dfree(s->bqoff);
+  dfree(s->bqbase);
+  dfree(s->bqkey);
+  dfree(s->btile);
+  dfree(s->bst);
+  hfree(s->bst_host);
+  dfree(s->bout);
   delete s;
 }
 
@@ -1048,10 +1124,10 @@ extern "C" int dawn_mssp_batch(dawn_solver_t s, const int64_t* sources, int64_t 
   const int64_t nb = (k + BL - 1) / BL;
   if (stats_out && s->bst_host_cap < nb) {
     CK(cudaStreamSynchronize(st));  // a previous asynchronous call may still write the old buffer
-    cudaFreeHost(s->bst_host);
+    hfree(s->bst_host);
     s->bst_host = nullptr;
     s->bst_host_cap = 0;
-    CK(cudaMallocHost(&s->bst_host, sizeof(BState) * nb));
+    CK(hmalloc(&s->bst_host, sizeof(BState) * nb));
     s->bst_host_cap = nb;
   }
   const size_t es = out_vtype == DAWN_F64 ? 8 : 4;
@@ -1083,7 +1159,7 @@ extern "C" int dawn_mssp(dawn_solver_t s, const int64_t* sources, int64_t k, int
   cudaStream_t st = (cudaStream_t)stream;
   CK(cudaSetDevice(s->g->device));
   DevState* hs = nullptr;
-  if (stats_out && k > 0) CK(cudaMallocHost(&hs, sizeof(DevState) * k));
+  if (stats_out && k > 0) CK(hmalloc(&hs, sizeof(DevState) * k));
   const int64_t n = s->g->n;
   int rc = DAWN_OK;
   for (int64_t i = 0; i < k && rc == DAWN_OK; ++i) {
@@ -1101,7 +1177,7 @@ extern "C" int dawn_mssp(dawn_solver_t s, const int64_t* sources, int64_t k, int
   }
   if (rc == DAWN_OK && hs)
     for (int64_t i = 0; i < k; ++i) fill_stats(hs[i], stats_out + i);
-  if (hs) cudaFreeHost(hs);
+  if (hs) hfree(hs);
   return rc;
 }
 
@@ -1144,8 +1220,12 @@ extern "C" int dawn_build_csr(int device, int64_t n, int64_t m, const int64_t* u
   const size_t out_bytes = out_dev ? 0 : 8 * (size_t)(n + 1) + 16 * (size_t)m;
   const size_t total = in_bytes + 32 * (size_t)m + out_bytes + tmp_bytes + 64;
   char* ws = nullptr;
-  CK(cudaMalloc(&ws, total));
-  auto release = [&](int rc) { cudaFree(ws); return rc; };
+  CK(dmalloc(&ws, total));
+  auto release = [&](int rc) {
+    cudaStreamSynchronize(st);
+    dfree(ws);
+    return rc;
+  };
   char* q = ws;
   const int64_t* du = u;
   const int64_t* dv = v;
