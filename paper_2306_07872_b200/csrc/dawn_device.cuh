@@ -297,6 +297,7 @@ struct DevState {
   unsigned long long wround[2];  // nodes lowered in the round with this parity
   unsigned tile_ctr[2];          // dynamic tile counters (relax pass)
   unsigned tile_ctr2[2];         // dynamic tile counters (predecessor pass)
+  unsigned sctr[2];              // dense S phase: chunks claimed beyond the first two per CTA, by round parity
   unsigned bar;                  // grid barrier word (never reset)
   unsigned round;                // next round to run (1 = seeding round)
   unsigned dense_prev;           // round-1 recorded its writes densely (stamps only)

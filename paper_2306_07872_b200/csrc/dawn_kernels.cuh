@@ -102,6 +102,7 @@ struct __align__(16) Smem {
   WarpRows<XI> w[WPB];
   unsigned long long scr64[WPB];
   unsigned long long basepk;
+  uint32_t claim[2];  // dense S phase: the chunk after next (double-buffered by iteration)
 };
 
 template <class V> struct EdgeAccess;
@@ -256,12 +257,19 @@ __device__ void phase_compact(const KParams<V, EI>& P, int p, uint32_t r, Smem<V
       o.rp[ITEMS] = (u + ITEMS <= n) ? __ldg(P.row_ptr + u + ITEMS) : (EI)0;
     }
   };
+  // Chunks: the first two per CTA are static (blockIdx.x, + gridDim.x), the
+  // rest are claimed from a counter one chunk ahead of the prefetch, so CTAs
+  // that drew cheap chunks take more (a hub chunk costs ~3x a typical one;
+  // static striding left the slowest CTA ~40 % behind the median).
   Pre nx;
-  if (blockIdx.x < nchunks) load_chunk(blockIdx.x, nx);
-  for (uint32_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+  uint32_t c = blockIdx.x, cn = blockIdx.x + gridDim.x;
+  if (c < nchunks) load_chunk(c, nx);
+  for (uint32_t it = 0; c < nchunks; ++it) {
     const uint32_t u0 = c * TILE + threadIdx.x * ITEMS;
     const Pre cur = nx;
-    if (c + gridDim.x < nchunks) load_chunk(c + gridDim.x, nx);
+    if (cn < nchunks) load_chunk(cn, nx);
+    uint32_t claim = nchunks;  // issued now, consumed (stored) only before the last barrier below
+    if (threadIdx.x == 0 && cn < nchunks) claim = 2u * gridDim.x + atomicAdd(&P.st->sctr[p], 1u);
     const K (&keys)[ITEMS] = cur.keys;
     const EI (&rp)[ITEMS + 1] = cur.rp;
     const bool full = u0 + ITEMS <= n;
@@ -306,7 +314,10 @@ __device__ void phase_compact(const KParams<V, EI>& P, int p, uint32_t r, Smem<V
     const unsigned long long mine = ((unsigned long long)mycnt << eb) | (unsigned long long)mydeg;
     unsigned long long tot;
     const unsigned long long incl = block_incl_sum<unsigned long long>(mine, s.scr64, &tot);
-    if (threadIdx.x == 0 && tot != 0ull) s.basepk = atomicAdd(&P.st->res[p], tot);
+    if (threadIdx.x == 0) {
+      if (tot != 0ull) s.basepk = atomicAdd(&P.st->res[p], tot);
+      s.claim[it & 1] = claim;
+    }
     __syncthreads();
     if (sel) {
       const unsigned long long at = s.basepk + incl - mine;
@@ -326,6 +337,8 @@ __device__ void phase_compact(const KParams<V, EI>& P, int p, uint32_t r, Smem<V
         }
       }
     }
+    c = cn;
+    cn = s.claim[it & 1];  // written before this iteration's barriers
   }
 }
 
@@ -1176,6 +1189,7 @@ __global__ void __launch_bounds__(NT, DAWN_MIN_BLOCKS) dawn_persistent(KParams<V
       if (leader) {
         st->res[p ^ 1] = 0ull;  // queue of round r+1 (filled by X_r or S_{r+1})
         st->wround[p] = 0ull;   // writes of round r (counted in X_r or S_{r+1})
+        st->sctr[p ^ 1] = 0u;   // chunk counter of S_{r+1} (S_{r-1} used it and is over)
       }
       if (r >= 2 && (dense_prev || P.algo == 1)) {
         uint32_t prev_w = 0;
@@ -1302,6 +1316,7 @@ __global__ void dawn_init_solve(KParams<V, EI> P) {
     P.qoff[1][0] = 0;
     P.qbase[1][0] = a;
     st->wround[0] = st->wround[1] = 0ull;
+    st->sctr[0] = st->sctr[1] = 0u;
     st->round = 1u;
     st->dense_prev = 0u;
     st->resume_x = 0u;

@@ -241,13 +241,25 @@ def _schedule_flag(schedule: str | None) -> int:
     return N.F_ASYNC if sch == "async" else 0
 
 
+def _host_array(shape, dtype=np.float64) -> np.ndarray:
+    """A numpy array in pinned (page-locked) host memory from torch's caching
+    host allocator: the device writes results into it at full PCIe speed, no
+    page faults, and the block returns to the cache when the array dies (a
+    config-2 distance vector: 0.6 ms instead of ~7 ms into fresh pageable
+    memory)."""
+    import torch
+
+    tdt = {np.dtype(np.float64): torch.float64, np.dtype(np.int64): torch.int64}[np.dtype(dtype)]
+    return torch.empty(shape, dtype=tdt, pin_memory=True).numpy()
+
+
 def _solve(g, source: int, algo: int, record_pred: bool, precision: str | None, schedule: str | None = None):
     _check_source(g, int(source))
     dg = device_graph(g, precision=precision)
     flags = (N.F_PRED if record_pred else 0) | _neg_flags(dg) | _schedule_flag(schedule)
     with dg.lock:
         s = dg.solver(flags)
-        dist = np.empty(dg.n, dtype=np.float64)
+        dist = _host_array(dg.n)
         pred = np.empty(dg.n, dtype=np.int64) if record_pred else None
         st = N.Stats()
         N.check(N.lib().dawn_sssp(s, int(source), algo, flags, dist.ctypes.data,
@@ -385,7 +397,7 @@ def _mssp_on_device(g, sources: list[int], algo: int, device: int, precision: st
     dg = device_graph(g, device=device, precision=precision)
     flags = _neg_flags(dg) | _schedule_flag(schedule)
     n = dg.n
-    rows = np.empty((len(sources), n), dtype=np.float64)
+    rows = _host_array((len(sources), n))
     stats = (N.Stats * max(len(sources), 1))()
     chunk = max(1, _ROW_BYTES_BUDGET // (8 * max(n, 1)))
     with dg.lock:
