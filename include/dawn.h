@@ -236,6 +236,16 @@ int dawn_gen_rmat(int device, int scale, int64_t edge_factor, double a, double b
                   uint64_t seed, int wkind, int64_t wlo, int64_t whi, uint64_t wseed,
                   int64_t* u_out, int64_t* v_out, double* w_out, void* stream);
 
+/* Dense all-pairs Floyd–Warshall on the device: floyd_warshall_apsp
+ * (oracles.py:141-162), the cross-check oracle, float64, same step order and
+ * rounding as the NumPy loop (not blocked).  Input: the CsrGraph arrays
+ * (int64 row_ptr[n+1], int64 col[m], float64 val[m]; host or device).
+ * out: float64[n][n] row-major, host or device.  *negative_cycle_out = any
+ * diagonal entry < 0.  The n-size cap (GraphSizeError) is the caller's.
+ * Synchronises `stream`. */
+int dawn_floyd_warshall(int device, int64_t n, const int64_t* row_ptr, const int64_t* col, const double* val,
+                        double* out, int* negative_cycle_out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -141,3 +141,26 @@ def rmat_csr(scale: int, edge_factor: int, weights: str = "int", lo: int = 1, hi
     if rc:
         raise MemoryError("oracle_rmat_csr failed")
     return n, m, rp, col, val
+
+
+def floyd_warshall(n: int, row_ptr, col, val) -> tuple[np.ndarray, bool]:
+    """CPU restatement (test infrastructure only) of the reference's dense
+    Floyd–Warshall, oracles.py:141-162: +inf matrix with a zero diagonal,
+    the minimum over parallel edges / self-loops, then for k = 0..n-1 every
+    entry takes min(D[i][j], D[i][k] + D[k][j]) with row and column k as
+    they were BEFORE step k (the reference forms the whole sum matrix first).
+    Returns (matrix, any diagonal entry < 0)."""
+    d = np.full((n, n), np.inf)
+    d[np.arange(n), np.arange(n)] = 0.0
+    rp = np.asarray(row_ptr, dtype=np.int64)
+    u = np.repeat(np.arange(n), np.diff(rp))
+    for a, b, w in zip(u.tolist(), np.asarray(col).tolist(), np.asarray(val, dtype=np.float64).tolist()):
+        if w < d[a, b]:
+            d[a, b] = w
+    for k in range(n):
+        colk = d[:, k].copy()
+        rowk = d[k, :].copy()
+        cand = colk[:, None] + rowk[None, :]
+        better = cand < d
+        d[better] = cand[better]
+    return d, bool(n and np.any(np.diagonal(d) < 0))

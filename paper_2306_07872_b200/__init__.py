@@ -42,7 +42,22 @@ from .solver import (
     seed_source,
 )
 
+from .errors import (
+    GraphParseError,
+    GraphSizeError,
+    NegativeWeightError,
+    SparsepathError,
+    UnsupportedFormatError,
+)
 from .experiments import MuReport, run_mu_experiment
+from .oracles import (
+    DEFAULT_FLOYD_CAP,
+    FloydResult,
+    OracleResult,
+    bellman_ford_sssp,
+    dijkstra_sssp,
+    floyd_warshall_apsp,
+)
 
 __version__ = "0.1.0"
 
@@ -78,4 +93,15 @@ __all__ = [
     "get_default_schedule",
     "MuReport",
     "run_mu_experiment",
+    "SparsepathError",
+    "GraphParseError",
+    "UnsupportedFormatError",
+    "NegativeWeightError",
+    "GraphSizeError",
+    "OracleResult",
+    "FloydResult",
+    "dijkstra_sssp",
+    "bellman_ford_sssp",
+    "floyd_warshall_apsp",
+    "DEFAULT_FLOYD_CAP",
 ]

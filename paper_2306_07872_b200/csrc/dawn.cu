@@ -26,6 +26,7 @@
 #include "../../include/dawn.h"
 #include "dawn_batch.cuh"
 #include "dawn_csr.cuh"
+#include "dawn_fw.cuh"
 
 using namespace dawn;
 
@@ -1339,4 +1340,69 @@ extern "C" int dawn_gen_rmat(int device, int scale, int64_t edge_factor, double 
                                                         u_out, v_out, w_out);
   CK(cudaGetLastError());
   return DAWN_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Floyd–Warshall on the device (floyd_warshall_apsp, oracles.py:141-162)
+// ---------------------------------------------------------------------------
+extern "C" int dawn_floyd_warshall(int device, int64_t n, const int64_t* row_ptr, const int64_t* col,
+                                   const double* val, double* out, int* negative_cycle_out, void* stream) {
+  if (n < 0) return fail(DAWN_EINVAL, "n must be >= 0");
+  if (n > 0 && (!row_ptr || !out)) return fail(DAWN_EINVAL, "NULL argument");
+  if (negative_cycle_out) *negative_cycle_out = 0;
+  if (n == 0) return DAWN_OK;
+  if (n > (1ll << 31)) return fail(DAWN_EUNSUPPORTED, "n=%lld too large for a dense matrix", (long long)n);
+  CK(cudaSetDevice(device));
+  cudaStream_t st = (cudaStream_t)stream;
+  int64_t m = 0;
+  CK(cudaMemcpy(&m, row_ptr + n, sizeof(int64_t), cudaMemcpyDefault));
+  if (m < 0) return fail(DAWN_EINVAL, "row_ptr[n] must be >= 0");
+  if (m > 0 && (!col || !val)) return fail(DAWN_EINVAL, "NULL argument");
+  const size_t nn = (size_t)n * (size_t)n;
+  char* ws = nullptr;
+  const size_t in_bytes = 8 * (size_t)(n + 1) + 16 * (size_t)m;
+  const size_t bytes = 8 * nn + 32 * (size_t)n + in_bytes + 64;
+  CK(dmalloc(&ws, bytes));
+  auto release = [&](int rc) {
+    cudaStreamSynchronize(st);
+    dfree(ws);
+    return rc;
+  };
+  unsigned long long* D = (unsigned long long*)ws;
+  double* colb = (double*)(ws + 8 * nn);
+  double* rowb = colb + 2 * n;
+  int64_t* d_rp = (int64_t*)(rowb + 2 * n);
+  int64_t* d_col = d_rp + (n + 1);
+  double* d_val = (double*)(d_col + m);
+  unsigned* flags = (unsigned*)(d_val + m);  // [0] barrier, [1] bad column, [2] negative diagonal
+  cudaError_t e;
+  if ((e = cudaMemcpyAsync(d_rp, row_ptr, 8 * (size_t)(n + 1), cudaMemcpyDefault, st)) != cudaSuccess ||
+      (m && (e = cudaMemcpyAsync(d_col, col, 8 * (size_t)m, cudaMemcpyDefault, st)) != cudaSuccess) ||
+      (m && (e = cudaMemcpyAsync(d_val, val, 8 * (size_t)m, cudaMemcpyDefault, st)) != cudaSuccess) ||
+      (e = cudaMemsetAsync(flags, 0, 16, st)) != cudaSuccess)
+    return release(fail(DAWN_ECUDA, "upload: %s", cudaGetErrorString(e)));
+  int nsm = 0, bps = 0;
+  CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
+  const int eb = (int)std::min<int64_t>((int64_t)nsm * 8, std::max<int64_t>(1, ((int64_t)nn + 255) / 256));
+  fw_init<<<eb, 256, 0, st>>>(D, n);
+  fw_edges<<<(int)std::min<int64_t>((int64_t)nsm * 8, (n + 255) / 256), 256, 0, st>>>(D, n, d_rp, d_col, d_val,
+                                                                                      flags + 1);
+  fw_decode<<<eb, 256, 0, st>>>(D, n, colb, rowb);
+  if ((e = cudaGetLastError()) != cudaSuccess) return release(fail(DAWN_ECUDA, "init: %s", cudaGetErrorString(e)));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, fw_steps, 256, 0));
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)bps * nsm, ((int64_t)nn + 255) / 256));
+  double* M = (double*)D;
+  unsigned* bar = flags;
+  void* args[] = {&M, &n, &colb, &rowb, &bar};
+  if ((e = cudaLaunchCooperativeKernel((void*)fw_steps, dim3(grid), dim3(256), args, 0, st)) != cudaSuccess)
+    return release(fail(DAWN_ECUDA, "steps: %s", cudaGetErrorString(e)));
+  fw_negdiag<<<(int)std::min<int64_t>(nsm * 4, (n + 255) / 256), 256, 0, st>>>(M, n, flags + 2);
+  unsigned hf[3] = {0, 0, 0};
+  if ((e = cudaMemcpyAsync(out, M, 8 * nn, cudaMemcpyDefault, st)) != cudaSuccess ||
+      (e = cudaMemcpyAsync(hf, flags, 12, cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
+      (e = cudaStreamSynchronize(st)) != cudaSuccess)
+    return release(fail(DAWN_ECUDA, "floyd-warshall: %s", cudaGetErrorString(e)));
+  if (hf[1]) return release(fail(DAWN_EINVAL, "column index out of range"));
+  if (negative_cycle_out) *negative_cycle_out = hf[2] ? 1 : 0;
+  return release(DAWN_OK);
 }
