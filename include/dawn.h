@@ -246,6 +246,15 @@ int dawn_gen_rmat(int device, int scale, int64_t edge_factor, double a, double b
 int dawn_floyd_warshall(int device, int64_t n, const int64_t* row_ptr, const int64_t* col, const double* val,
                         double* out, int* negative_cycle_out, void* stream);
 
+/* Distance rows as text, host side (format_distance_row, solver.py:498-506):
+ * for each of the k rows (row r at rows + r*ld, float64[n], host memory) one
+ * line "source,d0,...,d{n-1}\n" with "%.17g" values and the literal "inf"
+ * (and "nan" / "-inf" as Python prints them), concatenated into `out`.
+ * cap must be >= k * (24 + 26n) (else DAWN_EINVAL and *len_out = the bound);
+ * *len_out = bytes written.  threads <= 0: all hardware threads. */
+int dawn_format_rows(const double* rows, int64_t k, int64_t n, int64_t ld, const int64_t* sources, char* out,
+                     int64_t cap, int64_t* len_out, int threads);
+
 #ifdef __cplusplus
 }
 #endif

@@ -36,10 +36,13 @@ from .solver import (
     aggregate_stats,
     apsp,
     format_distance_row,
+    format_distance_rows,
     govm_sssp,
     gsvm_sssp,
     mssp,
+    read_distance_rows,
     seed_source,
+    write_distance_rows,
 )
 
 from .errors import (
@@ -82,6 +85,9 @@ __all__ = [
     "apsp",
     "aggregate_stats",
     "format_distance_row",
+    "format_distance_rows",
+    "write_distance_rows",
+    "read_distance_rows",
     "SOLVERS",
     "DeviceGraph",
     "device_graph",

@@ -57,6 +57,7 @@ EXPORTS = (
     "dawn_solver_cta_profile",
     "dawn_solver_worklist_stats",
     "dawn_floyd_warshall",
+    "dawn_format_rows",
     "dawn_mssp",
     "dawn_batch_supported",
     "dawn_mssp_batch",
@@ -108,6 +109,8 @@ def _declare(L: ctypes.CDLL) -> None:
         "dawn_solver_worklist_stats": (c_int, [c_void_p, c_void_p, c_void_p]),
         "dawn_floyd_warshall": (c_int, [c_int, c_int64, c_void_p, c_void_p, c_void_p, c_void_p, POINTER(c_int),
                                         c_void_p]),
+        "dawn_format_rows": (c_int, [c_void_p, c_int64, c_int64, c_int64, c_void_p, c_void_p, c_int64,
+                                     POINTER(c_int64), c_int]),
         "dawn_mssp": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_uint, c_void_p, c_void_p, c_void_p]),
         "dawn_batch_supported": (c_int, [c_void_p, c_int, c_uint, POINTER(c_int)]),
         "dawn_mssp_batch": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_uint, c_void_p, c_int, c_int64,

@@ -541,5 +541,65 @@ def _apsp_pipelined(g, name: str, sink, precision, batch: int, agg: AggregateSta
 
 
 def format_distance_row(dv: DistanceVector) -> str:
-    """``source,d0,d1,...`` with ``%.17g`` and the literal ``inf`` (solver.py:498-506)."""
-    return ",".join([str(dv.source)] + ["inf" if d == inf else "%.17g" % d for d in dv.dist.tolist()])
+    """``source,d0,d1,...`` with ``%.17g`` and the literal ``inf`` (solver.py:498-506).
+
+    Long rows go through the native multi-threaded formatter
+    (``dawn_format_rows``, same text byte for byte)."""
+    dist = np.asarray(dv.dist, dtype=np.float64)
+    if dist.size >= 2048:
+        return format_distance_rows(dist[None, :], [dv.source])[:-1]
+    return ",".join([str(dv.source)] + ["inf" if d == inf else "%.17g" % d for d in dist.tolist()])
+
+
+def format_distance_rows(rows, sources, threads: int = 0) -> str:
+    """Rows ``[k][n]`` (float64, any row stride) as ``k`` lines of
+    :func:`format_distance_row` text, each ending in a newline (SURVEY §8(f)
+    F2: the APSP text output path, ~20-40x the Python loop on 16 threads)."""
+    rows = np.asarray(rows, dtype=np.float64)
+    if rows.ndim != 2 or rows.strides[1] != 8:
+        rows = np.ascontiguousarray(rows, dtype=np.float64).reshape(len(sources), -1)
+    k, n = rows.shape
+    src = np.ascontiguousarray([int(x) for x in sources], dtype=np.int64)
+    if src.size != k:
+        raise ValueError("one source per row")
+    cap = k * (24 + 26 * n)
+    buf = ctypes.create_string_buffer(max(cap, 1))
+    ln = ctypes.c_int64(0)
+    ld = rows.strides[0] // 8 if k > 1 else n  # a single row may carry a 0 stride (x[None, :])
+    N.check(N.lib().dawn_format_rows(rows.ctypes.data, k, n, ld, src.ctypes.data, buf, cap, byref(ln),
+                                     int(threads)))
+    return buf.raw[: ln.value].decode("ascii")
+
+
+_ROWS_MAGIC = b"DAWNROWS"
+
+
+def write_distance_rows(fh, rows, sources, fmt: str = "text") -> int:
+    """Stream rows to a file object: ``text`` = :func:`format_distance_rows`
+    lines; ``binary`` = ``b"DAWNROWS"``, int64 k, int64 n, int64 sources[k],
+    float64 rows[k][n] little-endian (no formatting cost, exact values).
+    Returns the bytes written."""
+    rows = np.asarray(rows, dtype=np.float64)
+    if fmt == "text":
+        data = format_distance_rows(rows, sources).encode("ascii")
+        fh.write(data)
+        return len(data)
+    if fmt != "binary":
+        raise ValueError(f"unknown row format {fmt!r}; expected 'text' or 'binary'")
+    k, n = rows.shape
+    src = np.ascontiguousarray([int(x) for x in sources], dtype="<i8")
+    parts = [_ROWS_MAGIC, np.array([k, n], dtype="<i8").tobytes(), src.tobytes(),
+             np.ascontiguousarray(rows, dtype="<f8").tobytes()]
+    for p_ in parts:
+        fh.write(p_)
+    return sum(len(p_) for p_ in parts)
+
+
+def read_distance_rows(fh) -> tuple[np.ndarray, np.ndarray]:
+    """Inverse of ``write_distance_rows(..., fmt="binary")``: (sources, rows)."""
+    if fh.read(8) != _ROWS_MAGIC:
+        raise ValueError("not a DAWNROWS stream")
+    k, n = np.frombuffer(fh.read(16), dtype="<i8").tolist()
+    src = np.frombuffer(fh.read(8 * k), dtype="<i8").copy()
+    rows = np.frombuffer(fh.read(8 * k * n), dtype="<f8").reshape(k, n).copy()
+    return src, rows
