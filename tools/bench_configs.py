@@ -69,10 +69,29 @@ def main():
         st = N.Stats()
         N.check(L.dawn_solver_result(s, dist.ctypes.data, None, ctypes.byref(st), stream))
         vt = N.VTYPE_NAMES[dg.vtype]
+        # the async schedule on the same graph: time it and check its distances / flag
+        ta = []
+        for _ in range(a.solves):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            N.check(L.dawn_sssp_begin(s, src, N.GOVM, flags | N.F_ASYNC, stream))
+            N.check(L.dawn_sssp_run(s, 0, stream))
+            e1.record()
+            torch.cuda.synchronize()
+            ta.append(e0.elapsed_time(e1))
+        da = np.empty(g.n, np.float64)
+        sa = N.Stats()
+        N.check(L.dawn_solver_result(s, da.ctypes.data, None, ctypes.byref(sa), stream))
+        same = bool(np.array_equal(da, dist)) and bool(sa.negative_cycle) == bool(st.negative_cycle) and \
+            int(sa.first_discoveries) == int(st.first_discoveries)
+        if not bool(st.negative_cycle) and not same:
+            raise AssertionError("async schedule disagrees with the Jacobi solve")
+        async_rec = {"async_ms_median": statistics.median(ta), "async_relaxations": int(sa.relaxations),
+                     "async_equal_to_jacobi": same}
         dg.close()
-        return statistics.median(ts), ts, dist, st, vt
+        return statistics.median(ts), ts, dist, st, vt, async_rec
 
-    def record(name, g, src, ms, ts, dist, st, vt, parity, cpu=None, extra=None):
+    def record(name, g, src, ms, ts, dist, st, vt, async_rec, parity, cpu=None, extra=None):
         deg = np.diff(g.row_ptr)
         m_reach = int(deg[np.isfinite(dist)].sum())
         R, W = int(st.relaxations), int(st.writes)
@@ -85,6 +104,8 @@ def main():
                "early_exit": bool(st.early_exit), "gteps_mreach": m_reach / ms / 1e6,
                "relax_gps": R / ms / 1e6, "roofline_frac": b_alg / (ms / 1e3) / 1e9 / hbm,
                "us_per_round": 1e3 * ms / max(int(st.outer_steps), 1), "parity": parity, "cpu_baseline": cpu}
+        rec.update(async_rec)
+        rec["async_gteps_mreach"] = m_reach / async_rec["async_ms_median"] / 1e6
         if extra:
             rec.update(extra)
         results.append(rec)
@@ -108,17 +129,17 @@ def main():
     only = set(a.only.split(","))
     if "c1" in only:
         g = rmat_host(14, 8, "int")
-        ms, ts, dist, st, vt = device_solve(g, 0, "auto", False)
+        ms, ts, dist, st, vt, ar = device_solve(g, 0, "auto", False)
         od, _, o = O.jacobi_sssp(g, 0, "govm", vtype=vt)
         gd, go, cpu = cpu_time(g, 0)
         parity = {"dist_vs_jacobi_oracle": bool(np.array_equal(dist, od)),
                   "counters_vs_jacobi_oracle": (st.relaxations, st.writes, st.outer_steps) ==
                   (o["relaxations"], o["writes"], o["outer_steps"]),
                   "dist_vs_reference_order_port": bool(np.array_equal(dist, gd))}
-        record("c1: RMAT-14 ef8 int 1..100", g, 0, ms, ts, dist, st, vt, parity, cpu)
+        record("c1: RMAT-14 ef8 int 1..100", g, 0, ms, ts, dist, st, vt, ar, parity, cpu)
     if "c2" in only:
         g = rmat_host(22, 16, "f32")
-        ms, ts, dist, st, vt = device_solve(g, 0, "fp32", False)
+        ms, ts, dist, st, vt, ar = device_solve(g, 0, "fp32", False)
         od, _, o = O.jacobi_sssp(g, 0, "govm", vtype="float32")
         gd, go, cpu = cpu_time(g, 0)
         fin = np.isfinite(gd)
@@ -128,12 +149,12 @@ def main():
                   (o["relaxations"], o["writes"], o["outer_steps"]),
                   "reached_set_vs_reference_order_port": bool(np.array_equal(np.isfinite(dist), fin)),
                   "max_rel_err_vs_fp64_reference_order": rel, "tolerance": 1e-6}
-        record("c2: RMAT-22 ef16 fp32 U[0,1)", g, 0, ms, ts, dist, st, vt, parity, cpu)
+        record("c2: RMAT-22 ef16 fp32 U[0,1)", g, 0, ms, ts, dist, st, vt, ar, parity, cpu)
         del g
     if "c4" in only:
         k = a.grid
         g = G.grid_graph(k, k)
-        ms, ts, dist, st, vt = device_solve(g, 0, "auto", False)
+        ms, ts, dist, st, vt, ar = device_solve(g, 0, "auto", False)
         t0 = time.perf_counter()
         od, _, o = O.jacobi_sssp(g, 0, "govm", vtype=vt)
         t_or = time.perf_counter() - t0
@@ -142,7 +163,7 @@ def main():
                   (o["relaxations"], o["writes"], o["outer_steps"])}
         # reference-order port on the 1024^2 twin (full size is hours of CPU)
         tw = G.grid_graph(1024, 1024)
-        _, _, _, stw, _ = device_solve(tw, 0, "auto", False)
+        _, _, _, stw, _, _ = device_solve(tw, 0, "auto", False)
         gd, go, cpu = cpu_time(tw, 0)
         twd = np.empty(tw.n)
         dgt = DeviceGraph.from_csr(tw)
@@ -151,13 +172,13 @@ def main():
         dgt.close()
         parity["twin_1024_dist_vs_reference_order_port"] = bool(np.array_equal(twd, gd))
         cpu["sample"] = "reference-order govm on the 1024x1024 twin (full 4096^2 is hours on one core)"
-        record(f"c4: {k}x{k} grid int 1..100", g, 0, ms, ts, dist, st, vt, parity, cpu,
+        record(f"c4: {k}x{k} grid int 1..100", g, 0, ms, ts, dist, st, vt, ar, parity, cpu,
                {"jacobi_oracle_seconds": t_or})
         del g
     if "c5a" in only or "c5b" in only:
         base, pot = G.johnson_reweight(rmat_host(18, 16, "int"), pseed=3)
         if "c5a" in only:
-            ms, ts, dist, st, vt = device_solve(base, 0, "auto", True)
+            ms, ts, dist, st, vt, ar = device_solve(base, 0, "auto", True)
             od, _, o = O.jacobi_sssp(base, 0, "govm", vtype=vt, negcheck=True)
             gd, go, cpu = cpu_time(base, 0)
             parity = {"dist_vs_jacobi_oracle": bool(np.array_equal(dist, od)),
@@ -165,18 +186,18 @@ def main():
                       (o["relaxations"], o["writes"], o["outer_steps"]),
                       "dist_vs_reference_order_port": bool(np.array_equal(dist, gd)),
                       "negative_edges": int((base.val < 0).sum())}
-            record("c5a: RMAT-18 ef16 Johnson-negative int, no cycle", base, 0, ms, ts, dist, st, vt, parity, cpu)
+            record("c5a: RMAT-18 ef16 Johnson-negative int, no cycle", base, 0, ms, ts, dist, st, vt, ar, parity, cpu)
         if "c5b" in only:
             for kc, reach in ((1, True), (4, True), (1, False)):
                 cg = G.inject_cycles(base, kc, source=0, seed=7, reachable=reach)
-                ms, ts, dist, st, vt = device_solve(cg, 0, "auto", True)
+                ms, ts, dist, st, vt, ar = device_solve(cg, 0, "auto", True)
                 od, _, o = O.jacobi_sssp(cg, 0, "govm", vtype=vt, negcheck=True)
                 parity = {"flag_expected": reach, "flag_vs_jacobi_oracle": bool(st.negative_cycle) ==
                           bool(o["negative_cycle"]) == reach,
                           "counters_vs_jacobi_oracle": (st.relaxations, st.writes, st.outer_steps) ==
                           (o["relaxations"], o["writes"], o["outer_steps"])}
                 record(f"c5b: c5a + {kc} {'reachable' if reach else 'unreachable'} negative cycle(s)", cg, 0, ms, ts,
-                       dist, st, vt, parity, None,
+                       dist, st, vt, ar, parity, None,
                        {"note": "early exit by the predecessor-graph cycle check; the reference runs its n-round "
                                 "cap (n = 262144 rounds)"})
     if a.out:
