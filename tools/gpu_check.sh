@@ -30,6 +30,11 @@ if [[ $what == all || $what == ncu || $what == ncu_c2 ]]; then
     -o gpurun_out/prof_c2 -f python tools/round_profile.py --solves 3 > gpurun_out/ncu_full.log 2>&1
   echo "ncu c2 rc=$?"
 fi
+if [[ $what == ncu_wl ]]; then
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:dawn_worklist -s 2 -c 1 \
+    -o gpurun_out/prof_wl -f python tools/round_profile.py --solves 3 > gpurun_out/ncu_wl.log 2>&1
+  echo "ncu worklist rc=$?"
+fi
 if [[ $what == all || $what == ncu || $what == ncu_batch ]]; then
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:dawn_batch_persistent -s 3 -c 1 \
     -o gpurun_out/prof_batch -f python tools/apsp_probe.py --k 128 --single 2 > gpurun_out/ncu_batch.log 2>&1
