@@ -129,7 +129,7 @@ int dawn_solver_destroy(dawn_solver_t s);
  *   "bitmap_frontier" (default -1 = auto): 1 / 0 forces / disables the
  *   bitmap frontier of light rounds (auto: average out-degree < 8 and
  *   n >= 4096, narrow tiles; never with predecessors).
- *   "worklist_edges" (default 2^17; 0 = off): under DAWN_F_ASYNC, on graphs
+ *   "worklist_edges" (default 2^20; 0 = off): under DAWN_F_ASYNC, on graphs
  *   without negative weights, GOVM, unbounded runs, once a round relaxes
  *   fewer edges than this the rest of the solve runs barrier-free (a ring of
  *   row items taken by all warps).  Distances, negative_cycle and

@@ -167,7 +167,7 @@ struct dawn_solver_s {
   unsigned long long* wl_ring = nullptr;  // worklist tail (graphs without negative weights)
   uint64_t wl_cap = 0;
   int wl_grid = 1;
-  double worklist_edges = 1 << 17;        // tunable: async rounds relaxing < this many edges end the solve barrier-free (0 = off)
+  double worklist_edges = 1 << 20;        // tunable: async rounds relaxing < this many edges end the solve barrier-free (0 = off)
   DevState* st = nullptr;
   DevState* st_host = nullptr;  // pinned
   double* dbuf = nullptr;

@@ -873,11 +873,14 @@ __device__ __forceinline__ void wl_push(const KParams<V, EI>& P, const uint32_t 
   if (lane == 0) base = atomicAdd(&P.st->wl_ctr, ((unsigned long long)tot << 32) | tot);
   const uint32_t slot0 = (uint32_t)__shfl_sync(0xffffffffu, base, 0) + incl - mine;
   uint4* ring = reinterpret_cast<uint4*>(P.wl_ring);
+  // a slot below the ring size has not been used yet in this solve (every slot is empty when a
+  // solve starts): the lap check is only needed once the tickets wrap
+  const bool wrapped = (unsigned long long)(uint32_t)__shfl_sync(0xffffffffu, base, 0) + tot > P.wl_mask + 1ull;
   uint32_t pre[NJ];
   uint32_t t = 0;
 #pragma unroll
   for (int j = 0; j < NJ; ++j)  // all lap checks in flight at once
-    if ((msk >> j) & 1u) pre[j] = ld_relaxed_u32(&ring[(slot0 + t++) & P.wl_mask].x);
+    if ((msk >> j) & 1u) pre[j] = wrapped ? ld_relaxed_u32(&ring[(slot0 + t++) & P.wl_mask].x) : WL_NONE;
   t = 0;
 #pragma unroll
   for (int j = 0; j < NJ; ++j) {
@@ -888,12 +891,26 @@ __device__ __forceinline__ void wl_push(const KParams<V, EI>& P, const uint32_t 
   }
 }
 
+// A warp keeps up to 32 of the rows it lowered as its own next batch (no ring
+// round trip on the dependency chain: a hop costs edges -> gathers -> min);
+// the rest, and rows longer than one chunk, go to the ring for other warps.
+template <class K, class EI>
+struct WlLocal {
+  uint32_t node[32];
+  uint32_t deg[32];
+  K key[32];
+  EI a[32];
+};
+
 // relax edges [e0, e0 + len) (len <= 32*XI) of the rows held in lanes 0..nb-1
 // (first virtual edge off_k ascending, first real edge a_k, value val_k, every
-// row non-empty) and push the rows they lower.  Warp-collective.
+// row non-empty; rows flagged `skip` — undercut values — relax nothing) and
+// emit the rows they lower: into the warp's local list while it has room,
+// else to the ring.  Warp-collective.
 template <class V, class EI, int XI>
 __device__ __forceinline__ void wl_relax_tile(const KParams<V, EI>& P, uint32_t nb, uint32_t off, EI a,
-                                              typename Codec<V, true>::C val, uint32_t e0, uint32_t len,
+                                              typename Codec<V, true>::C val, bool skip, uint32_t e0, uint32_t len,
+                                              WlLocal<typename Codec<V, true>::K, EI>& L, uint32_t& ln,
                                               unsigned long long& acc_w, unsigned long long& acc_fd,
                                               unsigned long long& acc_multi) {
   using CD = Codec<V, true>;
@@ -920,8 +937,10 @@ __device__ __forceinline__ void wl_relax_tile(const KParams<V, EI>& P, uint32_t 
     const uint32_t x = e0 + lo + lane;
     const EI pos = __shfl_sync(0xffffffffu, a, k) + (EI)(x - __shfl_sync(0xffffffffu, off, k));
     rv[j] = __shfl_sync(0xffffffffu, val, k);
-    okm |= (unsigned)(lo + lane < len) << j;
-    if (lo + lane < len) EdgeAccess<V>::load(P, pos, col[j], wv[j]);
+    const bool live = lo + lane < len;
+    const bool sk = __shfl_sync(0xffffffffu, skip, k);  // every lane takes part in the shuffle
+    okm |= (unsigned)(live && !sk) << j;
+    if (live) EdgeAccess<V>::load(P, pos, col[j], wv[j]);
     else { col[j] = 0; wv[j] = 0; }
   }
   K cand[XI];
@@ -940,34 +959,83 @@ __device__ __forceinline__ void wl_relax_tile(const KParams<V, EI>& P, uint32_t 
     ra[j] = ok ? __ldg(P.row_ptr + col[j]) : (EI)0;
     rb[j] = ok ? __ldg(P.row_ptr + col[j] + 1) : (EI)0;
   }
-  unsigned low = 0;
+  // lower: a target that was +inf takes a returning min (first discoveries are counted exactly
+  // once); the others a fire-and-forget one.  The rows are emitted before any returned value is
+  // looked at (an item whose min lost the race is dropped by its taker as undercut).
+  unsigned need = 0, infm = 0;
   uint32_t dg[XI];
+  K old[XI];
 #pragma unroll
   for (int j = 0; j < XI; ++j) {
     dg[j] = (uint32_t)(rb[j] - ra[j]);
+    old[j] = 0;
     if (((okm >> j) & 1u) && cand[j] < cur[j]) {
       if (col[j] == P.src) { P.st->flag = 1u; continue; }
-      const uint32_t v = col[j];
-      unsigned* wsw = reinterpret_cast<unsigned*>(P.wstate + (v & ~3u));
-      const unsigned sh = 8u * (v & 3u);
-      bool lowered = true;
-      if (cur[j] == CD::INF) {  // maybe the first discovery: it must be counted exactly once
-        const K old = atomicMin(P.dist + v, cand[j]);
-        lowered = cand[j] < old;
-        if (old == CD::INF) { acc_fd++; atomicOr(wsw, 1u << sh); }
-        else if (lowered && !(atomicOr(wsw, 2u << sh) & (2u << sh))) acc_multi++;
+      need |= 1u << j;
+      if (cur[j] == CD::INF) {
+        infm |= 1u << j;
+        old[j] = atomicMin(P.dist + col[j], cand[j]);
       } else {
-        atomicMin(P.dist + v, cand[j]);  // fire and forget: cand < cur means it lowered dist[v] or a
-                                         // racing write went lower (then this item is dropped as stale)
-        if (!(atomicOr(wsw, 2u << sh) & (2u << sh))) acc_multi++;
-      }
-      if (lowered) {
-        acc_w++;
-        if (dg[j] > 0) low |= 1u << j;
+        atomicMin(P.dist + col[j], cand[j]);
       }
     }
   }
-  wl_push<V, EI, XI, K>(P, col, dg, cand, low, CH);
+  unsigned emit = 0, small = 0;
+#pragma unroll
+  for (int j = 0; j < XI; ++j) {
+    if (((need >> j) & 1u) && dg[j] > 0) {
+      emit |= 1u << j;
+      if (dg[j] <= CH) small |= 1u << j;
+    }
+  }
+  {  // local list first (rows of at most one chunk), the overflow and long rows to the ring
+    const uint32_t c = __popc(small);
+    const uint32_t incl = warp_incl_sum<uint32_t>(c);
+    const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+    const uint32_t room = 32u - ln;
+    uint32_t pos = incl - c;
+    unsigned ring_m = emit & ~small;
+#pragma unroll
+    for (int j = 0; j < XI; ++j) {
+      if ((small >> j) & 1u) {
+        if (pos < room) {
+          const uint32_t at = ln + pos;
+          L.node[at] = col[j];
+          L.deg[at] = dg[j];
+          L.key[at] = cand[j];
+          L.a[at] = ra[j];
+        } else {
+          ring_m |= 1u << j;
+        }
+        ++pos;
+      }
+    }
+    ln += min(tot, room);
+    __syncwarp();
+    wl_push<V, EI, XI, K>(P, col, dg, cand, ring_m, CH);
+  }
+  // bookkeeping from the returned values
+#pragma unroll
+  for (int j = 0; j < XI; ++j) {
+    if ((need >> j) & 1u) {
+      const uint32_t v = col[j];
+      unsigned* wsw = reinterpret_cast<unsigned*>(P.wstate + (v & ~3u));
+      const unsigned sh = 8u * (v & 3u);
+      if ((infm >> j) & 1u) {
+        if (old[j] == CD::INF) {
+          acc_fd++;
+          acc_w++;
+          atomicOr(wsw, 1u << sh);
+        } else if (cand[j] < old[j]) {
+          acc_w++;
+          if (!(atomicOr(wsw, 2u << sh) & (2u << sh))) acc_multi++;
+        }
+      } else {
+        acc_w++;
+        if (!(atomicOr(wsw, 2u << sh) & (2u << sh))) acc_multi++;
+      }
+    }
+  }
 }
 
 // round r's frontier (queue p) becomes the first items; the persistent kernel
@@ -1002,76 +1070,107 @@ __global__ void __launch_bounds__(NT, 2) dawn_worklist(KParams<V, EI> P) {
   unsigned long long acc_w = 0, acc_fd = 0, acc_multi = 0, acc_e = 0, acc_i = 0;
   const unsigned long long t_begin = globaltimer();
   unsigned long long busy = 0, nbatch = 0;
-  unsigned own = 0;  // claimed slots h + lane not taken yet
+  __shared__ WlLocal<K, EI> locs[WPB];
+  WlLocal<K, EI>& L = locs[threadIdx.x >> 5];
+  uint32_t ln = 0;    // rows in this warp's local list (warp-uniform)
+  uint32_t held = 0;  // ring items taken and not yet retired (they keep pending > 0 for the local chain)
+  unsigned own = 0;   // claimed slots h + lane not taken yet
   uint32_t h = 0;
   unsigned ns = 32;
   unsigned long long t0 = 0;
   for (;;) {
-    if (own == 0) {
-      uint32_t c = 1;
-      if (lane == 0) {
-        const uint32_t tail = (uint32_t)ld_relaxed(&st->wl_ctr), head = (uint32_t)ld_relaxed(&st->wl_head);
-        const uint32_t avail = tail - head;
-        c = (avail < 0x80000000u) ? min(32u, max(1u, avail / nw)) : 1u;
-        h = (uint32_t)atomicAdd(&st->wl_head, (unsigned long long)c);
-      }
-      c = __shfl_sync(0xffffffffu, c, 0);
-      h = __shfl_sync(0xffffffffu, h, 0);
-      own = (c >= 32) ? 0xFFFFFFFFu : ((1u << c) - 1u);
-    }
-    uint4* q = ring + ((h + lane) & P.wl_mask);
-    uint4 it = make_uint4(WL_NONE, WL_NONE, WL_NONE, WL_NONE);
-    if ((own >> lane) & 1u) it = ld_relaxed_v4(q);
-    // filled = both 8-byte halves written (w, the key's high word, is <= 0x7FFFFFFF in a real item)
-    const unsigned got = __ballot_sync(0xffffffffu, it.x != WL_NONE && it.w != WL_NONE);
-    if (got == 0) {
-      bool fin = false;
-      if (lane == 0) {
-        fin = (ld_relaxed(&st->wl_ctr) >> 32) == 0ull;
-        const unsigned long long t = globaltimer();
-        if (t0 == 0) t0 = t;
-        else if (t - t0 > 30ull * 1000000000ull) asm volatile("trap;");
-      }
-      if (__shfl_sync(0xffffffffu, fin, 0)) break;
-      __nanosleep(ns);
-      if (ns < 256) ns <<= 1;
-      continue;
-    }
-    ns = 32;
-    t0 = 0;
-    const unsigned long long t_got = globaltimer();
-    own &= ~got;
-    const bool mine = (got >> lane) & 1u;
-    if (mine) st_relaxed_v4(q, make_uint4(WL_NONE, WL_NONE, WL_NONE, WL_NONE));
-    const uint32_t u = it.x, y = it.y;
-    const K key = (K)(((unsigned long long)it.w << 32) | it.z);
-    // single-chunk rows: first edge and the stale check (a lower value was pushed separately)
+    unsigned got;
+    uint32_t u = 0, y = 0;
+    K key = 0;
     EI a = 0;
-    K now = key;
+    bool have_a = false;
+    unsigned long long t_got;
+    if (ln > 0) {
+      // ---- the rows this warp lowered itself: no ring round trip ----
+      got = (ln >= 32) ? 0xFFFFFFFFu : ((1u << ln) - 1u);
+      if (lane < ln) {
+        u = L.node[lane];
+        y = L.deg[lane];
+        key = L.key[lane];
+        a = L.a[lane];
+      }
+      have_a = true;
+      ln = 0;
+      __syncwarp();
+      t_got = globaltimer();
+    } else {
+      if (held) {  // back to the ring: retire what the local chain grew from (its pushes are counted)
+        if (lane == 0) atomicAdd(&st->wl_ctr, wl_retire(held));
+        held = 0;
+      }
+      if (own == 0) {
+        uint32_t c = 1;
+        if (lane == 0) {
+          const uint32_t tail = (uint32_t)ld_relaxed(&st->wl_ctr), head = (uint32_t)ld_relaxed(&st->wl_head);
+          const uint32_t avail = tail - head;
+          c = (avail < 0x80000000u) ? min(32u, max(1u, avail / nw)) : 1u;
+          h = (uint32_t)atomicAdd(&st->wl_head, (unsigned long long)c);
+        }
+        c = __shfl_sync(0xffffffffu, c, 0);
+        h = __shfl_sync(0xffffffffu, h, 0);
+        own = (c >= 32) ? 0xFFFFFFFFu : ((1u << c) - 1u);
+      }
+      uint4* q = ring + ((h + lane) & P.wl_mask);
+      uint4 it = make_uint4(WL_NONE, WL_NONE, WL_NONE, WL_NONE);
+      if ((own >> lane) & 1u) it = ld_relaxed_v4(q);
+      // filled = both 8-byte halves written (w, the key's high word, is <= 0x7FFFFFFF in a real item)
+      got = __ballot_sync(0xffffffffu, it.x != WL_NONE && it.w != WL_NONE);
+      if (got == 0) {
+        bool fin = false;
+        if (lane == 0) {
+          fin = (ld_relaxed(&st->wl_ctr) >> 32) == 0ull;
+          const unsigned long long t = globaltimer();
+          if (t0 == 0) t0 = t;
+          else if (t - t0 > 30ull * 1000000000ull) asm volatile("trap;");
+        }
+        if (__shfl_sync(0xffffffffu, fin, 0)) break;
+        __nanosleep(ns);
+        if (ns < 128) ns <<= 1;
+        continue;
+      }
+      ns = 32;
+      t0 = 0;
+      t_got = globaltimer();
+      own &= ~got;
+      if ((got >> lane) & 1u) st_relaxed_v4(q, make_uint4(WL_NONE, WL_NONE, WL_NONE, WL_NONE));
+      u = it.x;
+      y = it.y;
+      key = (K)(((unsigned long long)it.w << 32) | it.z);
+      held += __popc(got);
+    }
+    const bool mine = (got >> lane) & 1u;
+    // single-chunk rows: first edge; the undercut check runs beside the edge loads
     const bool single = mine && y <= CH;
+    K now = key;
     if (single) {
-      a = __ldg(P.row_ptr + u);
+      if (!have_a) a = __ldg(P.row_ptr + u);
       now = ldcg(P.dist + u);
     }
-    // drop only an item whose value was undercut (a lower write pushed its own item); a value above
-    // the item's means the item's own fire-and-forget min has not landed yet
-    const unsigned sm = __ballot_sync(0xffffffffu, single && !(now < key));
+    const unsigned sm = __ballot_sync(0xffffffffu, single);
     if (sm) {
       const uint32_t nb = __popc(sm);
       const uint32_t fl = (lane < nb) ? __fns(sm, 0, lane + 1) : 0u;
       const EI ra = __shfl_sync(0xffffffffu, a, fl);
       const uint32_t rd = __shfl_sync(0xffffffffu, y, fl);
       const K rk = __shfl_sync(0xffffffffu, key, fl);
+      // drop (relax nothing for) a row whose value was undercut: a lower write emitted its own row;
+      // a value above the row's means the row's own fire-and-forget min has not landed yet
+      const bool skip = __shfl_sync(0xffffffffu, now < key, fl);
       const uint32_t rdeg = (lane < nb) ? rd : 0u;
       const uint32_t incl = warp_incl_sum<uint32_t>(rdeg);
       const uint32_t Eb = __shfl_sync(0xffffffffu, incl, 31);
       const uint32_t off = incl - rdeg;
       const C val = CD::dec(rk);
       for (uint32_t e0 = 0; e0 < Eb; e0 += CH)
-        wl_relax_tile<V, EI, XI>(P, nb, off, ra, val, e0, min(CH, Eb - e0), acc_w, acc_fd, acc_multi);
+        wl_relax_tile<V, EI, XI>(P, nb, off, ra, val, skip, e0, min(CH, Eb - e0), L, ln, acc_w, acc_fd, acc_multi);
       if (lane == 0) acc_e += Eb;
     }
-    // long rows: split items and chunks, one at a time
+    // long rows (ring only): split items and chunks, one at a time
     unsigned lm = __ballot_sync(0xffffffffu, mine && y > CH);
     while (lm) {
       const int l = __ffs(lm) - 1;
@@ -1079,7 +1178,7 @@ __global__ void __launch_bounds__(NT, 2) dawn_worklist(KParams<V, EI> P) {
       const uint32_t lu = __shfl_sync(0xffffffffu, u, l), ly = __shfl_sync(0xffffffffu, y, l);
       const K lk = __shfl_sync(0xffffffffu, key, l);
       const EI la = __ldg(P.row_ptr + lu), lb = __ldg(P.row_ptr + lu + 1);
-      if (ldcg(P.dist + lu) < lk) continue;  // undercut: a lower write pushed its own item
+      if (ldcg(P.dist + lu) < lk) continue;  // undercut: a lower write emitted its own row
       if (ly == WL_SPLIT) {
         const uint32_t nch = (uint32_t)((lb - la + (EI)CH - 1) / (EI)CH);
         unsigned long long base = 0;
@@ -1093,14 +1192,13 @@ __global__ void __launch_bounds__(NT, 2) dawn_worklist(KParams<V, EI> P) {
       } else {
         const EI e0 = la + (EI)(ly & ~WL_CHUNK) * (EI)CH;
         const uint32_t len = (lb - e0 < (EI)CH) ? (uint32_t)(lb - e0) : CH;
-        wl_relax_tile<V, EI, XI>(P, 1u, 0u, e0, CD::dec(lk), 0u, len, acc_w, acc_fd, acc_multi);
+        wl_relax_tile<V, EI, XI>(P, 1u, 0u, e0, CD::dec(lk), false, 0u, len, L, ln, acc_w, acc_fd, acc_multi);
         if (lane == 0) acc_e += len;
       }
     }
     __syncwarp();
     if (lane == 0) {
       acc_i += __popc(got);
-      atomicAdd(&st->wl_ctr, wl_retire(__popc(got)));  // after this warp's pushes
       busy += globaltimer() - t_got;
       nbatch++;
     }

@@ -16,7 +16,7 @@ from paper_2306_07872_b200 import generators as G
 
 pytestmark = pytest.mark.gpu
 
-DEFAULT = float(1 << 17)
+DEFAULT = float(1 << 20)
 
 
 @pytest.fixture(params=[0.0, DEFAULT, 1e18], ids=["off", "default", "always"])
