@@ -225,6 +225,8 @@ __device__ void phase_compact(const KParams<V, EI>& P, int p, uint32_t r, Smem<V
   const uint32_t nchunks = (n + TILE - 1) / TILE;
   const bool gsvm = P.algo == 1;
   const int eb = P.ebits;
+  // keys: the snapshot values (Jacobi) and GSVM's finite test; the async schedule's GOVM needs neither
+  const bool need_keys = gsvm || !P.live;
   // Everything a chunk needs — stamps, write states, keys, row bounds — is
   // loaded one iteration ahead, unconditionally: a CTA walks ~7 chunks per
   // phase and a per-chunk chain of dependent loads (stamps -> keys/rows/state)
@@ -241,7 +243,11 @@ __device__ void phase_compact(const KParams<V, EI>& P, int p, uint32_t r, Smem<V
     const uint32_t u = c * TILE + threadIdx.x * ITEMS;
     if (u + ITEMS <= n) {
       ldcg8<uint32_t>(P.stamp + u, o.st);
-      ldcg8<K>(P.dist + u, o.keys);
+      if (need_keys) ldcg8<K>(P.dist + u, o.keys);
+      else {
+#pragma unroll
+        for (int j = 0; j < ITEMS; ++j) o.keys[j] = (K)0;  // GOVM + live rows: a stamped node is finite
+      }
       ldg8<EI>(P.row_ptr + u, *reinterpret_cast<EI(*)[ITEMS]>(o.rp));
       o.rp[ITEMS] = __ldg(P.row_ptr + u + ITEMS);
       o.ws = __ldcg(reinterpret_cast<const uint2*>(P.wstate + u));
@@ -250,7 +256,7 @@ __device__ void phase_compact(const KParams<V, EI>& P, int p, uint32_t r, Smem<V
 #pragma unroll
       for (int j = 0; j < ITEMS; ++j) {
         o.st[j] = (u + j < n) ? ldcg(P.stamp + u + j) : 0u;
-        o.keys[j] = (u + j < n) ? ldcg(P.dist + u + j) : VT::INF;
+        o.keys[j] = (u + j < n) ? (need_keys ? ldcg(P.dist + u + j) : (K)0) : VT::INF;
         o.rp[j] = (u + j <= n) ? __ldg(P.row_ptr + u + j) : (EI)0;
         b[j] = (u + j < n) ? ldcg(P.wstate + u + j) : (uint8_t)0;
       }
