@@ -401,6 +401,12 @@ def ours(args):
     fin = torch.isfinite(dist_dev)
     m_reach = int(deg[fin].sum().item())
     R, Wr, steps_run = int(st.relaxations), int(st.writes), int(st.outer_steps)
+    import ctypes
+
+    wl = (ctypes.c_uint64 * 6)()
+    N.check(L.dawn_solver_worklist_stats(s, wl, stream))
+    worklist = ({"from_round": int(wl[0]), "items": int(wl[1]), "warp_batches": int(wl[2]),
+                 "span_us": wl[5] / 1e3} if wl[1] else None)
     t_step = tot_ms / K / 1e3
     value = world * m_reach / t_step / 1e9
 
@@ -549,6 +555,7 @@ def ours(args):
         "gpu_launches": (3 if sflag else 2) * K,
         "clocks": clocks,
         "relax_gps": world * R / t_step / 1e9,
+        "worklist": worklist,
         "solve": {"rounds": steps_run, "relaxations": R, "writes": Wr, "first_discoveries": int(st.first_discoveries),
                   "m_reach": m_reach, "n": n, "m": dg.m},
     }
