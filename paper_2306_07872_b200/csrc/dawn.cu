@@ -356,6 +356,73 @@ static int convert_graph(dawn_graph_t g, const int64_t* d_rp, const int64_t* d_c
   return DAWN_OK;
 }
 
+// Host-resident inputs of real size: the edge arrays cross PCIe by DMA in
+// chunks into two device staging slots while the previous chunk converts on a
+// second stream (copy engine and SMs overlap; zero-copy reads of pinned memory
+// reached ~51 GB/s against ~55 GB/s for the DMA).
+template <class V>
+static int convert_graph_staged(dawn_graph_t g, const int64_t* h_rp, const int64_t* h_col, const double* h_val,
+                                unsigned* d_flags) {
+  const int64_t n = g->n, m = g->m;
+  constexpr int64_t CHE = 1ll << 22;  // edges per chunk (64 MB of col + val)
+  const int blocks = 148 * 8;
+  char* stage = nullptr;
+  const size_t slot = 16 * (size_t)std::min<int64_t>(CHE, m);
+  CK(dmalloc(&stage, 8 * (size_t)(n + 1) + 2 * slot));
+  cudaStream_t cs = nullptr, ks = nullptr;
+  cudaEvent_t copied[2] = {nullptr, nullptr}, used[2] = {nullptr, nullptr};
+  auto finish = [&](int rc) {
+    if (ks) cudaStreamSynchronize(ks);
+    if (cs) cudaStreamSynchronize(cs);
+    for (int i = 0; i < 2; ++i) {
+      if (copied[i]) cudaEventDestroy(copied[i]);
+      if (used[i]) cudaEventDestroy(used[i]);
+    }
+    if (cs) cudaStreamDestroy(cs);
+    if (ks) cudaStreamDestroy(ks);
+    dfree(stage);
+    return rc;
+  };
+  cudaError_t e;
+  if ((e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking)) != cudaSuccess ||
+      (e = cudaStreamCreateWithFlags(&ks, cudaStreamNonBlocking)) != cudaSuccess)
+    return finish(fail(DAWN_ECUDA, "streams: %s", cudaGetErrorString(e)));
+  for (int i = 0; i < 2; ++i)
+    if ((e = cudaEventCreateWithFlags(&copied[i], cudaEventDisableTiming)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&used[i], cudaEventDisableTiming)) != cudaSuccess)
+      return finish(fail(DAWN_ECUDA, "events: %s", cudaGetErrorString(e)));
+  // the flags were cleared on the legacy stream, which these non-blocking streams do not follow
+  if ((e = cudaStreamSynchronize(0)) != cudaSuccess)
+    return finish(fail(DAWN_ECUDA, "graph upload: %s", cudaGetErrorString(e)));
+  // row pointers first (the monotonicity check reads the whole array)
+  int64_t* s_rp = (int64_t*)stage;
+  if ((e = cudaMemcpyAsync(s_rp, h_rp, 8 * (size_t)(n + 1), cudaMemcpyHostToDevice, ks)) != cudaSuccess)
+    return finish(fail(DAWN_ECUDA, "graph upload: %s", cudaGetErrorString(e)));
+  if (g->wide)
+    k_convert_rowptr<unsigned long long><<<blocks, 256, 0, ks>>>(s_rp, n, m, (unsigned long long*)g->row_ptr, d_flags);
+  else
+    k_convert_rowptr<uint32_t><<<blocks, 256, 0, ks>>>(s_rp, n, m, (uint32_t*)g->row_ptr, d_flags);
+  char* slots = stage + 8 * (size_t)(n + 1);
+  for (int64_t off = 0, c = 0; off < m; off += CHE, ++c) {
+    const int64_t len = std::min<int64_t>(CHE, m - off);
+    const int b = (int)(c & 1);
+    int64_t* s_col = (int64_t*)(slots + b * slot);
+    double* s_val = (double*)(s_col + std::min<int64_t>(CHE, m));
+    if (c >= 2 && (e = cudaStreamWaitEvent(cs, used[b], 0)) != cudaSuccess)
+      return finish(fail(DAWN_ECUDA, "graph upload: %s", cudaGetErrorString(e)));
+    if ((e = cudaMemcpyAsync(s_col, h_col + off, 8 * (size_t)len, cudaMemcpyHostToDevice, cs)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(s_val, h_val + off, 8 * (size_t)len, cudaMemcpyHostToDevice, cs)) != cudaSuccess ||
+        (e = cudaEventRecord(copied[b], cs)) != cudaSuccess || (e = cudaStreamWaitEvent(ks, copied[b], 0)) != cudaSuccess)
+      return finish(fail(DAWN_ECUDA, "graph upload: %s", cudaGetErrorString(e)));
+    k_convert_edges<V><<<blocks, 256, 0, ks>>>(s_col, s_val, len, n, g->e2 ? g->e2 + off : nullptr,
+                                               g->ecol ? g->ecol + off : nullptr, g->ew ? g->ew + off : nullptr,
+                                               d_flags);
+    if ((e = cudaGetLastError()) != cudaSuccess || (e = cudaEventRecord(used[b], ks)) != cudaSuccess)
+      return finish(fail(DAWN_ECUDA, "graph convert: %s", cudaGetErrorString(e)));
+  }
+  return finish(DAWN_OK);
+}
+
 static void graph_free(dawn_graph_t g) {
   if (!g) return;
   cudaSetDevice(g->device);
@@ -417,7 +484,10 @@ extern "C" int dawn_graph_create(int device, int64_t n, int64_t m, const int64_t
   unsigned* d_flags = nullptr;
   const bool pinned = !src_is_device && is_pinned_host_ptr(row_ptr) && (m == 0 || (is_pinned_host_ptr(col) &&
                                                                                    is_pinned_host_ptr(val)));
-  if (pinned) {
+  const bool staged = !src_is_device && m >= (1ll << 22);  // large host graphs: chunked DMA + convert
+  if (staged) {
+    // converted below by convert_graph_staged
+  } else if (pinned) {
     cudaPointerAttributes a;
     cudaPointerGetAttributes(&a, row_ptr);
     d_rp = (const int64_t*)a.devicePointer;
@@ -452,11 +522,20 @@ extern "C" int dawn_graph_create(int device, int64_t n, int64_t m, const int64_t
     return cleanup(fail(DAWN_ECUDA, "flags: %s", cudaGetErrorString(e)));
   }
   int rc = DAWN_OK;
-  switch (vtype) {
-    case DAWN_I32: rc = convert_graph<int32_t>(g, d_rp, d_col, d_val, d_flags); break;
-    case DAWN_I64: rc = convert_graph<int64_t>(g, d_rp, d_col, d_val, d_flags); break;
-    case DAWN_F32: rc = convert_graph<float>(g, d_rp, d_col, d_val, d_flags); break;
-    default: rc = convert_graph<double>(g, d_rp, d_col, d_val, d_flags); break;
+  if (staged) {
+    switch (vtype) {
+      case DAWN_I32: rc = convert_graph_staged<int32_t>(g, row_ptr, col, val, d_flags); break;
+      case DAWN_I64: rc = convert_graph_staged<int64_t>(g, row_ptr, col, val, d_flags); break;
+      case DAWN_F32: rc = convert_graph_staged<float>(g, row_ptr, col, val, d_flags); break;
+      default: rc = convert_graph_staged<double>(g, row_ptr, col, val, d_flags); break;
+    }
+  } else {
+    switch (vtype) {
+      case DAWN_I32: rc = convert_graph<int32_t>(g, d_rp, d_col, d_val, d_flags); break;
+      case DAWN_I64: rc = convert_graph<int64_t>(g, d_rp, d_col, d_val, d_flags); break;
+      case DAWN_F32: rc = convert_graph<float>(g, d_rp, d_col, d_val, d_flags); break;
+      default: rc = convert_graph<double>(g, d_rp, d_col, d_val, d_flags); break;
+    }
   }
   unsigned hflags = 0;
   if (rc == DAWN_OK) {
