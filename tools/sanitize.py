@@ -1,7 +1,9 @@
 """Small solves of every kernel family under compute-sanitizer (memcheck /
 racecheck / synccheck): single-source GOVM/GSVM on all value types, frontier
-modes and tile widths, predecessors + negative-cycle check, batched
-multi-source, device CSR build.
+modes and tile widths, both round schedules (async with the worklist tail off,
+at the default and from round 2 on), predecessors + negative-cycle check,
+batched multi-source (both schedules), device CSR build, device Floyd-Warshall,
+the chunked host-graph upload.
 
     compute-sanitizer --tool memcheck python tools/sanitize.py
 """
@@ -40,10 +42,16 @@ def main():
                 for algo in ("govm", "gsvm"):
                     P.SOLVERS[algo](g, 0, precision=prec)
                     checked += 1
+                for wl in (0.0, float(1 << 20), 1e18):  # async: tail off / default / from round 2
+                    P.set_tuning(worklist_edges=wl)
+                    P.govm_sssp(g, 0, precision=prec, schedule="async")
+                    checked += 1
+                P.set_tuning(worklist_edges=float(1 << 20))
             P.govm_sssp(g, 1, record_pred=True)
             MS.mssp_tile(g, list(range(40)), "govm")
+            MS.mssp_tile(g, list(range(40)), "govm", schedule="async")
             MS.mssp_tile(g, list(range(7)), "gsvm")
-            checked += 3
+            checked += 4
     P.set_tuning(dense_edges_per_node=0.5, wide_tiles=-1, bitmap_frontier=-1)
     for g in (neg, cyc):
         P.govm_sssp(g, 0)
@@ -53,7 +61,11 @@ def main():
     u = rng.integers(0, 1000, 20000)
     v = rng.integers(0, 1000, 20000)
     D.build_csr_device(1000, u, v, rng.uniform(0, 1, 20000))
-    print(f"sanitize: {checked} solves + batches + csr build ran")
+    P.floyd_warshall_apsp(graphs[0])
+    P.floyd_warshall_apsp(neg if neg.n <= 2000 else graphs[1])
+    big = G.rmat_graph(16, 80, weights="f32")  # m >= 2^22: chunked DMA upload path
+    P.govm_sssp(big, 0, precision="fp32", schedule="async")
+    print(f"sanitize: {checked} solves + batches + csr build + floyd-warshall + staged upload ran")
 
 
 if __name__ == "__main__":
