@@ -1083,7 +1083,7 @@ __global__ void __launch_bounds__(NT, 2) dawn_worklist(KParams<V, EI> P) {
   unsigned own = 0;   // claimed slots h + lane not taken yet
   uint32_t h = 0;
   unsigned ns = 32;
-  unsigned long long t0 = 0;
+  unsigned long long t0 = 0, seen = 0;
   for (;;) {
     unsigned got;
     uint32_t u = 0, y = 0;
@@ -1129,10 +1129,17 @@ __global__ void __launch_bounds__(NT, 2) dawn_worklist(KParams<V, EI> P) {
       if (got == 0) {
         bool fin = false;
         if (lane == 0) {
-          fin = (ld_relaxed(&st->wl_ctr) >> 32) == 0ull;
+          const unsigned long long ctr = ld_relaxed(&st->wl_ctr);
+          fin = (ctr >> 32) == 0ull;
+          // watchdog: trap only if the whole worklist made no progress (no push, no retire) for 30 s;
+          // waiting long while other warps work (a long dependency chain) is legitimate
           const unsigned long long t = globaltimer();
-          if (t0 == 0) t0 = t;
-          else if (t - t0 > 30ull * 1000000000ull) asm volatile("trap;");
+          if (t0 == 0 || ctr != seen) {
+            t0 = t;
+            seen = ctr;
+          } else if (t - t0 > 30ull * 1000000000ull) {
+            asm volatile("trap;");
+          }
         }
         if (__shfl_sync(0xffffffffu, fin, 0)) break;
         __nanosleep(ns);

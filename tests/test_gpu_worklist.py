@@ -132,3 +132,22 @@ def test_worklist_not_used_when_stepping(gpu):
         assert same(dv.dist, P.govm_sssp(g, 0)[0].dist)
     finally:
         P.set_tuning(worklist_edges=DEFAULT)
+
+
+def test_worklist_long_chain(gpu):
+    """A 20 000-hop dependency chain (8 parallel edges per hop, so the queue
+    frontier and the tail are used, not the bitmap frontier): the worklist runs
+    a long serial chain of local batches while every other warp waits."""
+    n = 20000
+    rng = np.random.default_rng(3)
+    u = np.repeat(np.arange(n - 1), 8)
+    v = u + 1
+    w = rng.integers(1, 9, u.size).astype(float)
+    # a few long-range shortcuts with large weights (never on the shortest path)
+    su = rng.integers(0, n, 2000)
+    sv = rng.integers(0, n, 2000)
+    g = P.csr_from_arrays(n, np.concatenate([u, su]), np.concatenate([v, sv]),
+                          np.concatenate([w, np.full(2000, 1e6)]))
+    da, _, sa = P.govm_sssp(g, 0, schedule="async")
+    od, _, _ = O.gs_sssp(g, 0)
+    assert same(da.dist, od)
