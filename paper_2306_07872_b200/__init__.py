@@ -53,6 +53,14 @@ from .errors import (
     UnsupportedFormatError,
 )
 from .experiments import MuReport, run_mu_experiment
+from .graphio import (
+    load_edge_list,
+    load_matrix_market,
+    read_graph,
+    write_edge_list,
+    write_graph,
+    write_matrix_market,
+)
 from .oracles import (
     DEFAULT_FLOYD_CAP,
     FloydResult,
@@ -110,4 +118,10 @@ __all__ = [
     "bellman_ford_sssp",
     "floyd_warshall_apsp",
     "DEFAULT_FLOYD_CAP",
+    "load_edge_list",
+    "load_matrix_market",
+    "write_edge_list",
+    "write_matrix_market",
+    "read_graph",
+    "write_graph",
 ]
