@@ -249,6 +249,9 @@ def _host_array(shape, dtype=np.float64) -> np.ndarray:
     memory)."""
     import torch
 
+    count = int(np.prod(shape)) if isinstance(shape, tuple) else int(shape)
+    if count * np.dtype(dtype).itemsize > (1 << 30):  # do not page-lock huge result sets
+        return np.empty(shape, dtype=dtype)
     tdt = {np.dtype(np.float64): torch.float64, np.dtype(np.int64): torch.int64}[np.dtype(dtype)]
     return torch.empty(shape, dtype=tdt, pin_memory=True).numpy()
 
