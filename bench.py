@@ -497,7 +497,8 @@ def ours(args):
         if not np.array_equal(np.isfinite(out_h.numpy()), fin.cpu().numpy()):
             raise AssertionError("C-ABI result disagrees with the timed device result")
         # resident graph through the Python API (upload cached, as the reference holds its CsrGraph)
-        P.govm_sssp(host, src, precision="fp32", schedule=args.schedule)
+        for _ in range(3):  # warm, in the timed loop's pattern (the result pool reaches its steady state)
+            dv, _, _st = P.govm_sssp(host, src, precision="fp32", schedule=args.schedule)
         torch.cuda.synchronize()
         KR = max(3, min(K, 20))
         t0 = time.perf_counter()
