@@ -552,7 +552,7 @@ def ours(args):
         "e2e": e2e,
         "e2e_resident": e2e_resident,
         "apsp": apsp,
-        # per step: dawn_init_solve + dawn_persistent (+ dawn_worklist under the async schedule)
+        # per step: dawn_begin_solve + dawn_persistent (+ dawn_worklist under the async schedule)
         "gpu_launches": (3 if sflag else 2) * K,
         "clocks": clocks,
         "relax_gps": world * R / t_step / 1e9,

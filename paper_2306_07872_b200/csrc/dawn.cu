@@ -680,15 +680,12 @@ struct Impl {
 
   static int begin(dawn_solver_t s, cudaStream_t stream) {
     const int64_t n = s->g->n;
-    CK(cudaMemsetAsync(s->dist, 0xFF, sizeof(K) * n, stream));
-    CK(cudaMemsetAsync(s->stamp, 0, sizeof(uint32_t) * n, stream));
-    CK(cudaMemsetAsync(s->bmap, 0, 4 * (size_t)((n + 31) / 32 + 4), stream));
-    CK(cudaMemsetAsync(s->wstate, 0, (size_t)n, stream));
     if (s->prof) CK(cudaMemsetAsync(s->prof, 0, 32 * (size_t)s->prof_cap, stream));
     if (s->pred) CK(cudaMemsetAsync(s->pred, 0, sizeof(unsigned long long) * n, stream));
     KParams<V, EI> P = params(s, 0);
-    if (s->g->has_negative) dawn_init_solve<V, EI, false><<<1, 32, 0, stream>>>(P);
-    else dawn_init_solve<V, EI, true><<<1, 32, 0, stream>>>(P);
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(148 * 8, (n + 255) / 256));
+    if (s->g->has_negative) dawn_begin_solve<V, EI, false><<<blocks, 256, 0, stream>>>(P);
+    else dawn_begin_solve<V, EI, true><<<blocks, 256, 0, stream>>>(P);
     CK(cudaGetLastError());
     return DAWN_OK;
   }

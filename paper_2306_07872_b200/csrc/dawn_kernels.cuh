@@ -1412,13 +1412,28 @@ __global__ void __launch_bounds__(NT, DAWN_MIN_BLOCKS) dawn_persistent(KParams<V
 // ---------------------------------------------------------------------------
 // small kernels
 // ---------------------------------------------------------------------------
-// solve init: seed frontier {source} with key 0 (solver.py:275-280, :343-350)
+// solve init (solver.py:275-280, :343-350), everything in one launch: dist =
+// INF with the source's key 0, stamps / write states / bitmap cleared, and
+// (block 0) the seed frontier {source} plus the solve state — instead of four
+// memsets and a launch (26 -> 12 us of a config-2 step)
 template <class V, class EI, bool RAW>
-__global__ void dawn_init_solve(KParams<V, EI> P) {
+__global__ void dawn_begin_solve(KParams<V, EI> P) {
+  using CD = Codec<V, RAW>;
+  using K = typename CD::K;
+  const uint32_t n = P.n;
+  const size_t T = (size_t)gridDim.x * blockDim.x;
+  const size_t t0 = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const K k0 = CD::enc((V)0);
+  for (size_t i = t0; i < n; i += T) {
+    P.dist[i] = (i == P.src) ? k0 : CD::INF;
+    P.stamp[i] = 0u;
+  }
+  uint32_t* ws = reinterpret_cast<uint32_t*>(P.wstate);  // allocated n + 4 bytes
+  for (size_t i = t0; i < ((size_t)n + 3) / 4; i += T) ws[i] = 0u;
+  for (size_t i = t0; i < ((size_t)n + 31) / 32 + 4; i += T) P.bmap[i] = 0u;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     DevState* st = P.st;
     const uint32_t s = P.src;
-    P.dist[s] = Codec<V, RAW>::enc((V)0);
     const EI a = P.row_ptr[s], b = P.row_ptr[s + 1];
     const unsigned long long deg = (unsigned long long)(b - a);
     st->res[0] = 0ull;
