@@ -9,15 +9,16 @@ per source on a fork pool and pickle float64 rows back to the parent.  Here:
   Graphs the batched kernel does not take (negative weights, predecessors)
   run one persistent solve per source — still on the GPU.
 * :func:`apsp_sharded` — one process per GPU (torchrun): the graph is
-  replicated in every HBM, source batches are dealt round-robin over ranks
-  (batch ``b`` -> rank ``b % world``), and every rank delivers its rows into
-  the root rank's tile in source order.  Transport ``"p2p"``: the root's
+  replicated in every HBM, ranks claim source batches dynamically from a
+  group-wide cursor (per-source cost varies by orders of magnitude), and
+  every rank delivers its rows into the root rank's tile at the batch's
+  offset, so the tile is in source order.  Transport ``"p2p"``: the root's
   tile is mapped into every rank through CUDA IPC and rows travel as
   copy-engine peer copies over NVLink on a side stream, overlapped with the
   next batch's kernel (no SMs taken from the persistent kernel).
   ``"collective"``: ``torch.distributed`` point-to-point (NCCL, or gloo on
-  CPU) after the compute.  Stats are gathered as host objects; the
-  ``negative_cycle`` flags travel with them.
+  CPU) after the compute.  Per-source counters and the ``negative_cycle``
+  flags travel in one ``all_reduce``; per-rank load in one ``all_gather``.
 """
 
 from __future__ import annotations
@@ -33,7 +34,8 @@ from .device import DeviceGraph, device_graph
 
 BATCH = 32  # sources per batched pass (warp lanes)
 
-__all__ = ["BATCH", "batch_supported", "mssp_tile", "apsp_sharded", "shard_batches", "ShardedResult"]
+__all__ = ["BATCH", "batch_supported", "mssp_tile", "apsp_sharded", "batch_bounds", "shard_batches", "BatchCursor",
+           "ShardedResult"]
 
 
 def _algo_id(algo: str) -> int:
@@ -116,25 +118,78 @@ def mssp_tile(g, sources: Sequence[int], algo: str = "govm", *, precision: str |
 
 
 # ---------------------------------------------------------------------------
-# sharding over ranks
+# sharding over ranks: dynamic batch claiming
 # ---------------------------------------------------------------------------
+def batch_bounds(k: int, batch: int = BATCH) -> list[tuple[int, int]]:
+    """Batch b = sources [b*batch, min(k, (b+1)*batch))."""
+    return [(lo, min(k, lo + batch)) for lo in range(0, k, batch)]
+
+
 def shard_batches(k: int, world: int, batch: int = BATCH) -> list[list[tuple[int, int]]]:
-    """Round-robin deal of source batches: rank r gets [(lo, hi), ...] with
-    batch b = [b*batch, min(k, (b+1)*batch)) assigned to rank b % world."""
+    """Static round-robin deal (batch b -> rank b % world); kept as the
+    ``claim="static"`` plan and for comparison with the dynamic cursor."""
     out: list[list[tuple[int, int]]] = [[] for _ in range(world)]
-    for b, lo in enumerate(range(0, k, batch)):
-        out[b % world].append((lo, min(k, lo + batch)))
+    for b, lohi in enumerate(batch_bounds(k, batch)):
+        out[b % world].append(lohi)
     return out
 
 
-@dataclass
-class ShardedResult:
-    tile: object | None          # root: [k][n] tensor, rows in source order; others: None
-    stats: list | None           # root: list[SolveStats] in source order
-    ms: float                    # this rank's device time (first launch -> rows delivered)
-    ms_max: float                # max over ranks
-    transport: str
-    batches: int                 # batches this rank solved
+class BatchCursor:
+    """A group-wide atomic batch counter: ``claim()`` returns the next
+    unclaimed batch index (>= the batch count once all are taken).
+
+    The counter lives in the process group's key-value store (rank 0's
+    TCPStore), so a claim is one ``add`` round trip (~0.1 ms) against a
+    ~8 ms batch solve; ranks that draw cheap sources simply come back sooner.
+    This is the reference's chunked pool hand-out (solver.py:453-457,
+    :487-494) across processes.  ``static`` deals ``b % world`` instead."""
+
+    _calls = 0
+
+    def __init__(self, nbatches: int, group=None, static: bool = False):
+        import torch.distributed as dist
+
+        self.nbatches = nbatches
+        self.static = static
+        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+        BatchCursor._calls += 1  # collective call order is the same on every rank
+        self.key = f"dawn/apsp/{BatchCursor._calls}"
+        self._next_static = self.rank
+        self.store = None
+        if not static:
+            from torch.distributed import distributed_c10d as c10d
+
+            self.store = c10d._get_default_store()
+
+    def claim(self) -> int:
+        if self.static:
+            b = self._next_static
+            self._next_static += self.world
+            return b
+        return int(self.store.add(self.key, 1)) - 1
+
+
+# native counters carried per source through the stats all-reduce
+_STAT_FIELDS = ("outer_steps", "relaxations", "writes", "first_discoveries", "multi_written", "negative_cycle",
+                "early_exit")
+
+
+def _stats_to_row(st) -> list[int]:
+    """A SolveStats (or native Stats) as the int64 row the all-reduce carries."""
+    if hasattr(st, "multi_written"):
+        return [int(getattr(st, f)) for f in _STAT_FIELDS]
+    fd = int(st.first_discoveries)
+    multi = int(round(st.updated_ratio * max(fd, 1)))
+    return [int(st.outer_steps), int(st.relaxations), int(st.writes), fd, multi, int(bool(st.negative_cycle)), 0]
+
+
+def _solve_stats_from_row(row) -> "object":
+    from .solver import _stats_from_native
+
+    st = N.Stats()
+    for f, v in zip(_STAT_FIELDS, row):
+        setattr(st, f, int(v))
+    return _stats_from_native(st)
 
 
 def _p2p_possible(root_dev: int, my_dev: int) -> bool:
@@ -148,17 +203,38 @@ def _p2p_possible(root_dev: int, my_dev: int) -> bool:
         return False
 
 
+@dataclass
+class ShardedResult:
+    tile: object | None          # root: [k][n] tensor, rows in source order; others: None
+    stats: list | None           # every rank: list[SolveStats] in source order (all-reduced)
+    ms: float                    # this rank's device time (first launch -> rows delivered)
+    ms_max: float                # max over ranks
+    transport: str
+    batches: int                 # batches this rank solved
+    claimed: list | None = None  # this rank's batch indices, in claim order
+    per_rank: list | None = None  # every rank: [{"rank", "batches", "sources", "busy_ms"}]
+
+
 def apsp_sharded(g, sources: Sequence[int], algo: str = "govm", *, precision: str | None = None,
                  group=None, root: int = 0, out_dtype=None, transport: str = "auto",
                  solve_fn: Callable | None = None, tile=None, ring: int = 3,
-                 schedule: str | None = None) -> ShardedResult:
+                 schedule: str | None = None, claim: str = "dynamic") -> ShardedResult:
     """Multi-source solve sharded over the ranks of ``group`` (one process per GPU).
 
-    Every rank must call it with the same ``g`` (replicated) and ``sources``.
-    ``solve_fn(lo, hi) -> (rows [hi-lo][n] tensor, list[SolveStats])``
-    replaces the device solve (tests drive the host logic with it on gloo).
-    ``tile``: optional preallocated root tile ``[k][n]`` (reused across calls).
+    Every rank must call it with the same ``g`` (replicated in every HBM) and
+    ``sources``.  Batches of :data:`BATCH` sources are claimed dynamically
+    from a group-wide cursor (:class:`BatchCursor`; ``claim="static"`` deals
+    them round-robin), each rank solves what it claims and delivers the rows
+    into the root's ``[k][n]`` tile at the batch's offset, so the tile is in
+    source order whatever rank solved a batch.  Per-source counters travel in
+    one ``all_reduce(SUM)`` of a ``[k][7]`` int64 tensor (every rank ends with
+    all stats; ``negative_cycle`` included), per-rank load in one
+    ``all_gather``.  ``solve_fn(lo, hi) -> (rows [hi-lo][n] tensor,
+    list[SolveStats-like])`` replaces the device solve (tests drive the host
+    logic with it on gloo); ``tile``: optional preallocated root tile.
     """
+    import time
+
     import torch
     import torch.distributed as dist
 
@@ -181,7 +257,11 @@ def apsp_sharded(g, sources: Sequence[int], algo: str = "govm", *, precision: st
     for s in src:
         if not 0 <= s < n:
             raise ValueError(f"source {s} out of range for n={n}")
-    mine = shard_batches(k, world)[rank]
+    if claim not in ("dynamic", "static"):
+        raise ValueError(f"unknown claim mode {claim!r}")
+    cdev = dev if backend == "nccl" else torch.device("cpu")  # collectives' device
+    bounds = batch_bounds(k)
+    cursor = BatchCursor(len(bounds), group, static=(claim == "static"))
 
     if transport == "auto":
         transport = "p2p" if on_gpu else "collective"
@@ -190,7 +270,7 @@ def apsp_sharded(g, sources: Sequence[int], algo: str = "govm", *, precision: st
         rdev = [dev.index if on_gpu else -1]
         dist.broadcast_object_list(rdev, src=root, group=group)
         ok = torch.tensor([1 if on_gpu and rdev[0] >= 0 and _p2p_possible(rdev[0], dev.index) else 0],
-                          device=dev if backend == "nccl" else "cpu")
+                          device=cdev)
         dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
         if int(ok.item()) == 0:
             transport = "collective"
@@ -198,15 +278,25 @@ def apsp_sharded(g, sources: Sequence[int], algo: str = "govm", *, precision: st
     if rank == root and tile is None:
         tile = torch.empty((k, n), dtype=out_dtype, device=dev)
 
+    stat_rows = torch.zeros((max(k, 1), len(_STAT_FIELDS)), dtype=torch.int64)
+
     def solve(lo, hi, out_rows):
         if solve_fn is not None:
             rows, st = solve_fn(lo, hi)
             out_rows.copy_(rows)
-            return st
-        _, st = mssp_tile(dg, src[lo:hi], algo, out=out_rows, out_dtype=out_dtype, stats=True, schedule=schedule)
-        return st
+        else:
+            _, st = mssp_tile(dg, src[lo:hi], algo, out=out_rows, out_dtype=out_dtype, stats=True,
+                              schedule=schedule)
+        stat_rows[lo:hi] = torch.tensor([_stats_to_row(x) for x in st], dtype=torch.int64)
 
-    stats_local: list[tuple[int, list]] = []
+    def claims():
+        while True:
+            b = cursor.claim()
+            if b >= len(bounds):
+                return
+            yield b
+
+    claimed: list[int] = []
     t0 = t1 = None
     if on_gpu:
         t0 = torch.cuda.Event(enable_timing=True)
@@ -215,6 +305,7 @@ def apsp_sharded(g, sources: Sequence[int], algo: str = "govm", *, precision: st
     if on_gpu:
         torch.cuda.synchronize(dev)
         t0.record()
+    w0 = time.perf_counter()
 
     if transport == "p2p":
         # map the root's tile into this process (CUDA IPC) -> copy-engine peer copies
@@ -230,15 +321,17 @@ def apsp_sharded(g, sources: Sequence[int], algo: str = "govm", *, precision: st
         cstream = torch.cuda.Stream(device=dev)
         ring_bufs = [torch.empty((BATCH, n), dtype=out_dtype, device=dev) for _ in range(ring)] if rank != root else []
         ring_done = [None] * len(ring_bufs)
-        for i, (lo, hi) in enumerate(mine):
+        for i, b in enumerate(claims()):
+            lo, hi = bounds[b]
+            claimed.append(b)
             if rank == root:
-                stats_local.append((lo, solve(lo, hi, tile[lo:hi])))
+                solve(lo, hi, tile[lo:hi])
                 continue
             slot = i % ring
             if ring_done[slot] is not None:
                 torch.cuda.current_stream(dev).wait_event(ring_done[slot])
             buf = ring_bufs[slot][: hi - lo]
-            stats_local.append((lo, solve(lo, hi, buf)))
+            solve(lo, hi, buf)
             ready = torch.cuda.Event()
             ready.record()
             with torch.cuda.stream(cstream):
@@ -250,16 +343,16 @@ def apsp_sharded(g, sources: Sequence[int], algo: str = "govm", *, precision: st
         if rank != root:
             cstream.synchronize()
     else:
-        # compute everything locally, then point-to-point to the root in batch order
+        # compute what this rank claims, then point-to-point to the root in claim order
         local = {}
-        for lo, hi in mine:
-            if rank == root:
-                rows = tile[lo:hi]
-            else:
-                rows = torch.empty((hi - lo, n), dtype=out_dtype, device=dev)
-            stats_local.append((lo, solve(lo, hi, rows)))
-            local[lo] = rows
-        plan = shard_batches(k, world)
+        for b in claims():
+            lo, hi = bounds[b]
+            claimed.append(b)
+            rows = tile[lo:hi] if rank == root else torch.empty((hi - lo, n), dtype=out_dtype, device=dev)
+            solve(lo, hi, rows)
+            local[b] = rows
+        plan = [None] * world
+        dist.all_gather_object(plan, claimed, group=group)
         # gloo moves host memory only: stage device rows through the host
         staged = on_gpu and backend != "nccl"
         if rank == root:
@@ -267,7 +360,8 @@ def apsp_sharded(g, sources: Sequence[int], algo: str = "govm", *, precision: st
             for r in range(world):
                 if r == root:
                     continue
-                for lo, hi in plan[r]:
+                for b in plan[r]:
+                    lo, hi = bounds[b]
                     buf = torch.empty((hi - lo, n), dtype=out_dtype) if staged else tile[lo:hi]
                     reqs.append((dist.irecv(buf, src=r, group=group), lo, hi, buf))
             for q, lo, hi, buf in reqs:
@@ -275,7 +369,7 @@ def apsp_sharded(g, sources: Sequence[int], algo: str = "govm", *, precision: st
                 if staged:
                     tile[lo:hi].copy_(buf)
         else:
-            reqs = [dist.isend(local[lo].cpu() if staged else local[lo], dst=root, group=group) for lo, _ in mine]
+            reqs = [dist.isend(local[b].cpu() if staged else local[b], dst=root, group=group) for b in claimed]
             for q in reqs:
                 q.wait()
     if on_gpu:
@@ -283,17 +377,20 @@ def apsp_sharded(g, sources: Sequence[int], algo: str = "govm", *, precision: st
         torch.cuda.synchronize(dev)
         ms = t0.elapsed_time(t1)
     else:
-        ms = 0.0
+        ms = 1e3 * (time.perf_counter() - w0)
     dist.barrier(group=group)  # every rank's rows are resident on the root
-    tm = torch.tensor([ms], dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
+    tm = torch.tensor([ms], dtype=torch.float64, device=cdev)
     dist.all_reduce(tm, op=dist.ReduceOp.MAX, group=group)
-    gathered = [None] * world if rank == root else None
-    dist.gather_object(stats_local, gathered, dst=root, group=group)
-    stats = None
-    if rank == root:
-        stats = [None] * k
-        for part in gathered:
-            for lo, sts in part:
-                stats[lo:lo + len(sts)] = sts
+    # per-source counters: each source solved by exactly one rank -> SUM = gather
+    st_red = stat_rows.to(cdev)
+    dist.all_reduce(st_red, op=dist.ReduceOp.SUM, group=group)
+    st_all = st_red.cpu().numpy()
+    stats = [_solve_stats_from_row(st_all[i]) for i in range(k)]
+    nsrc = sum(bounds[b][1] - bounds[b][0] for b in claimed)
+    load = torch.tensor([[rank, len(claimed), nsrc, ms]], dtype=torch.float64, device=cdev)
+    loads = [torch.empty_like(load) for _ in range(world)]
+    dist.all_gather(loads, load, group=group)
+    per_rank = [{"rank": int(x[0, 0]), "batches": int(x[0, 1]), "sources": int(x[0, 2]), "busy_ms": float(x[0, 3])}
+                for x in (t.cpu() for t in loads)]
     return ShardedResult(tile=tile if rank == root else None, stats=stats, ms=ms, ms_max=float(tm.item()),
-                         transport=transport, batches=len(mine))
+                         transport=transport, batches=len(claimed), claimed=claimed, per_rank=per_rank)

@@ -267,8 +267,6 @@ def _host_array(shape, dtype=np.float64) -> np.ndarray:
     always pageable (page-locking them would cost more than it saves)."""
     import weakref
 
-    import torch
-
     count = int(np.prod(shape)) if isinstance(shape, tuple) else int(shape)
     nbytes = count * np.dtype(dtype).itemsize
     with _PINNED_LOCK:
@@ -280,10 +278,18 @@ def _host_array(shape, dtype=np.float64) -> np.ndarray:
         _PINNED_LIVE[0] += 1
         _PINNED_LIVE[1] += nbytes
     if block is None:
-        block = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
-    arr = block.numpy().view(dtype).reshape(shape)
-    weakref.finalize(arr, _pinned_released, nbytes, block)
-    return arr
+        block = _new_pinned_block(nbytes)
+    # every view of the result (rows[i], dist[a:b], ...) has ``raw`` as its
+    # base, so the block goes back to the pool only when the last view dies
+    raw = block.numpy()
+    weakref.finalize(raw, _pinned_released, nbytes, block)
+    return raw.view(dtype).reshape(shape)
+
+
+def _new_pinned_block(nbytes: int):
+    import torch
+
+    return torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
 
 
 def _solve(g, source: int, algo: int, record_pred: bool, precision: str | None, schedule: str | None = None):
@@ -425,23 +431,22 @@ SOLVERS = {"gsvm": gsvm_sssp, "govm": govm_sssp}
 _ROW_BYTES_BUDGET = 1 << 30  # float64 rows copied back per dawn_mssp call
 
 
-def _mssp_on_device(g, sources: list[int], algo: int, device: int, precision: str | None,
-                    schedule: str | None = None):
+def _mssp_run(g, sources: list[int], algo: int, device: int, precision: str | None, schedule: str | None,
+              rows: np.ndarray, stats, claim: Callable[[], tuple[int, int] | None]) -> None:
+    """Solve the source ranges ``claim()`` hands out on one device, writing
+    rows ``[lo, hi)`` of ``rows`` (host float64) and ``stats``."""
     dg = device_graph(g, device=device, precision=precision)
     flags = _neg_flags(dg) | _schedule_flag(schedule)
-    n = dg.n
-    rows = _host_array((len(sources), n))
-    stats = (N.Stats * max(len(sources), 1))()
-    chunk = max(1, _ROW_BYTES_BUDGET // (8 * max(n, 1)))
     with dg.lock:
         s = dg.solver(flags)
-        for lo in range(0, len(sources), chunk):
-            part = np.asarray(sources[lo:lo + chunk], dtype=np.int64)
-            k = int(part.shape[0])
-            N.check(N.lib().dawn_mssp(s, part.ctypes.data, k, algo, flags, rows[lo:lo + k].ctypes.data,
+        while True:
+            rng = claim()
+            if rng is None:
+                return
+            lo, hi = rng
+            part = np.asarray(sources[lo:hi], dtype=np.int64)
+            N.check(N.lib().dawn_mssp(s, part.ctypes.data, hi - lo, algo, flags, rows[lo:hi].ctypes.data,
                                       ctypes.addressof(stats) + lo * ctypes.sizeof(N.Stats), dg.stream()))
-    return [(DistanceVector(dist=rows[i], source=int(src)), _stats_from_native(stats[i]))
-            for i, src in enumerate(sources)]
 
 
 def _devices_for(workers: int) -> list[int]:
@@ -456,9 +461,13 @@ def mssp(g, sources: Sequence[int], algo: str = "govm", workers: int = 1, *,
     """Independent solves from each source, results in the given order (solver.py:426-457).
 
     ``workers`` is the number of GPUs the sources are spread over (capped at
-    the visible device count); results are bit-identical for any value.
-    ``schedule`` as in :func:`gsvm_sssp` (``async``: same rows, per-source
-    counters timing-dependent).
+    the visible device count); results are bit-identical for any value.  With
+    several GPUs, one host thread per device claims source chunks from a
+    shared cursor (the reference's pool hands out chunks dynamically too,
+    solver.py:453-457): per-source cost varies by orders of magnitude, so a
+    static split would leave devices idle.  ``schedule`` as in
+    :func:`gsvm_sssp` (``async``: same rows, per-source counters
+    timing-dependent).
     """
     _schedule_flag(schedule)  # validate before any work
     name = _normalize_algo(algo)
@@ -471,17 +480,35 @@ def mssp(g, sources: Sequence[int], algo: str = "govm", workers: int = 1, *,
         return []
     algo_id = _ALGO[name]
     devs = _devices_for(workers)
-    if len(devs) == 1 or len(sources) == 1:
-        return _mssp_on_device(g, sources, algo_id, devs[0], precision, schedule)
-    # contiguous blocks, one host thread per GPU; order restored by block index
-    blocks = np.array_split(np.arange(len(sources)), len(devs))
-    with ThreadPoolExecutor(max_workers=len(devs)) as ex:
-        futs = [ex.submit(_mssp_on_device, g, [sources[i] for i in blk], algo_id, d, precision, schedule)
-                for d, blk in zip(devs, blocks) if len(blk)]
-        out = []
-        for f in futs:
-            out.extend(f.result())
-    return out
+    k, n = len(sources), int(g.n)
+    rows = _host_array((k, n))
+    stats = (N.Stats * k)()
+    if len(devs) == 1 or k == 1:
+        chunk = max(1, _ROW_BYTES_BUDGET // (8 * max(n, 1)))
+    else:
+        # ~8 claims per device, whole 32-source batches of the batched kernel
+        chunk = max(32, -(-k // (8 * len(devs)) // 32) * 32)
+    chunk = min(chunk, max(1, _ROW_BYTES_BUDGET // (8 * max(n, 1))))
+    cursor = [0]
+    lock = threading.Lock()
+
+    def claim():
+        with lock:
+            lo = cursor[0]
+            if lo >= k:
+                return None
+            cursor[0] = min(k, lo + chunk)
+            return lo, cursor[0]
+
+    if len(devs) == 1 or k == 1:
+        _mssp_run(g, sources, algo_id, devs[0], precision, schedule, rows, stats, claim)
+    else:
+        with ThreadPoolExecutor(max_workers=len(devs)) as ex:
+            for f in [ex.submit(_mssp_run, g, sources, algo_id, d, precision, schedule, rows, stats, claim)
+                      for d in devs]:
+                f.result()
+    return [(DistanceVector(dist=rows[i], source=src), _stats_from_native(stats[i]))
+            for i, src in enumerate(sources)]
 
 
 def apsp(g, algo: str = "govm", workers: int = 1, sink: Callable[[DistanceVector], None] | None = None, *,

@@ -121,3 +121,32 @@ def test_generate_random_graph_matches_reference_fixture():
         g = P.generate_random_graph(c["n"], c["avg_degree"], P.WeightMode.unit(), seed=c["graph_seed"])
         digest = hashlib.sha256(np.ascontiguousarray(g.row_ptr).tobytes() + np.ascontiguousarray(g.col).tobytes())
         assert digest.hexdigest() == c["graph_sha256"]
+
+
+def test_pinned_result_pool_keeps_live_views(monkeypatch):
+    """A pooled result block returns to the pool only when the last view of
+    the result dies (row views of an mssp result kept the block's
+    memory alive but not the array the finalizer watched)."""
+    import gc
+
+    import torch
+
+    from paper_2306_07872_b200 import solver as S
+
+    monkeypatch.setattr(S, "_new_pinned_block", lambda nbytes: torch.empty(nbytes, dtype=torch.uint8))
+    monkeypatch.setattr(S, "_PINNED_FREE", {})
+    monkeypatch.setattr(S, "_PINNED_LIVE", [0, 0])
+    rows = S._host_array((2, 3))
+    rows[:] = 1.0
+    views = [rows[0], rows[1][1:]]
+    del rows
+    gc.collect()
+    again = S._host_array((2, 3))  # must not reuse the block the views still point into
+    again[:] = 2.0
+    assert views[0].tolist() == [1.0, 1.0, 1.0] and views[1].tolist() == [1.0, 1.0]
+    del views
+    gc.collect()
+    assert S._PINNED_FREE.get(48), "the block goes back to the pool once every view is gone"
+    third = S._host_array(6)
+    third[:] = 3.0
+    assert again.tolist() == [[2.0] * 3] * 2

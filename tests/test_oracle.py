@@ -137,3 +137,59 @@ def test_jacobi_negcheck_verdict_matches_cap():
     unreach = G.inject_cycles(base, 1, source=0, seed=1, reachable=False)
     _, _, u = O.jacobi_sssp(unreach, 0, "govm", vtype="int64", negcheck=True)
     assert not u["negative_cycle"]
+
+
+# ---------------------------------------------------------------------------
+# full-scale pins: the reference package's own outputs on the BASELINE graphs
+# (tests/golden/scale_golden.json, made by tests/golden/make_scale_golden.py)
+# ---------------------------------------------------------------------------
+def _scale_golden():
+    import json
+
+    from conftest import GOLDEN
+
+    return json.loads((GOLDEN / "scale_golden.json").read_text())
+
+
+def _graph_sha(g) -> str:
+    h = hashlib.sha256()
+    for a, dt in ((g.row_ptr, np.int64), (g.col, np.int64), (g.val, np.float64)):
+        h.update(np.ascontiguousarray(a, dtype=dt).tobytes())
+    return h.hexdigest()
+
+
+@pytest.mark.parametrize("name", ["c2_src0", "c3_sample", "c5a_src0", "c5b12_reach", "c5b12_unreach",
+                                  "grid1024_src0"])
+def test_gs_port_equals_reference_at_scale(name):
+    """The reference-order port reproduces the reference package's distances
+    (sha256 of the float64 vector) and counters on the BASELINE-scale graphs:
+    the CPU baseline and the bench's parity check stand on it."""
+    import sys
+    from pathlib import Path
+
+    sys.path.insert(0, str(Path(__file__).resolve().parent / "golden"))
+    from make_scale_golden import build_case
+
+    case = _scale_golden()[name]
+    g, sources = build_case(name)
+    assert _graph_sha(g) == case["graph_sha256"]
+    assert sources == [r["source"] for r in case["runs"]]
+    for run in case["runs"]:
+        if run["stats"]["outer_steps"] == g.n and g.n > 4096:
+            continue  # a cap run (none at these sizes)
+        dist, _, st = O.gs_sssp(g, run["source"])
+        if not run["stats"]["negative_cycle"]:
+            assert hashlib.sha256(dist.tobytes()).hexdigest() == run["dist_sha256"]
+        assert _stats_ref_view(st) == run["stats"]
+
+
+def test_rmat_generators_agree_on_host():
+    """oracle rmat_csr (C, the reference arm's generator) == generators.rmat_graph (numpy restatement of
+    dawn_gen_rmat): the CPU baseline and the GPU arm solve the same graph."""
+    from paper_2306_07872_b200 import generators as G
+
+    for scale, ef, w in ((10, 8, "int"), (12, 16, "f32"), (14, 8, "int")):
+        n, m, rp, col, val = O.rmat_csr(scale, ef, weights=w)
+        g = G.rmat_graph(scale, ef, weights=w)
+        assert (n, m) == (g.n, g.m)
+        assert np.array_equal(rp, g.row_ptr) and np.array_equal(col, g.col) and np.array_equal(val, g.val)
