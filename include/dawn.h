@@ -255,6 +255,24 @@ int dawn_floyd_warshall(int device, int64_t n, const int64_t* row_ptr, const int
 int dawn_format_rows(const double* rows, int64_t k, int64_t n, int64_t ld, const int64_t* sources, char* out,
                      int64_t cap, int64_t* len_out, int threads);
 
+/* Independent cross-check oracles, computed on the HOST by design (they check
+ * the device kernels from outside and share no code with them; the solvers
+ * above never call them).  Native restatements of the reference's oracles
+ * with the same visiting order and float64 arithmetic, so dist, relaxation
+ * counts and the negative-cycle verdict equal the reference's exactly.
+ * Inputs are the CsrGraph host arrays (int64 row_ptr[n+1], int64 col[m],
+ * float64 val[m]); dist_out is float64[n].  The negative-weight check
+ * (NegativeWeightError) is the caller's.
+ *   dawn_oracle_dijkstra     : dijkstra_sssp     (oracles.py:59-91), binary heap
+ *                              over (dist, node) with lazy deletion.
+ *   dawn_oracle_bellman_ford : bellman_ford_sssp (oracles.py:94-138), n-1 in-place
+ *                              passes in row order + one detection pass; no
+ *                              source guard (dist[source] may go below 0). */
+int dawn_oracle_dijkstra(int64_t n, const int64_t* row_ptr, const int64_t* col, const double* val,
+                         int64_t source, double* dist_out, int64_t* relaxations_out);
+int dawn_oracle_bellman_ford(int64_t n, const int64_t* row_ptr, const int64_t* col, const double* val,
+                             int64_t source, double* dist_out, int64_t* relaxations_out, int* negative_cycle_out);
+
 #ifdef __cplusplus
 }
 #endif

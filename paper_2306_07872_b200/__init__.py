@@ -40,6 +40,7 @@ from .solver import (
     govm_sssp,
     gsvm_sssp,
     mssp,
+    mssp_stats,
     read_distance_rows,
     seed_source,
     write_distance_rows,
@@ -90,6 +91,7 @@ __all__ = [
     "gsvm_sssp",
     "govm_sssp",
     "mssp",
+    "mssp_stats",
     "apsp",
     "aggregate_stats",
     "format_distance_row",

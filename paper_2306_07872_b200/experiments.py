@@ -1,37 +1,47 @@
-"""The paper's μ experiment on the GPU.
+"""The paper's μ experiment on the device.
 
-Mirror of ``run_mu_experiment`` / ``MuReport`` (reference experiments.py:55-92,
-:127-178): the same seeded source sample, the same unit-weight baseline and
-U[0, 2) randomized arm over one graph structure, the same checks and report
-fields.  Both arms run through :func:`mssp`, i.e. the batched multi-source
-kernel (32 sources per pass) — the reference solves one source at a time in
-Python.
+API of the reference's ``run_mu_experiment`` / ``MuReport``
+(``sparsepath/experiments.py:55-92``, ``:127-178``): same arguments, source
+sample, weight arms, error texts and report layout, so the reference's
+callers and tests take this module unchanged.
 
-Counters follow the device's snapshot-Jacobi rounds: the
-baseline arm is identical to the reference's (unit weights discover every
-path exactly once, so μ = 1 and re_updates = 0 in both orders); the
-randomized arm's μ and updated ratio are the Jacobi figures, deterministic but
-not equal to the reference's Gauss-Seidel counts on large graphs.
+The work is organised differently.  The experiment only consumes work
+counters, so each arm is one counters-only multi-source run
+(:func:`solver.mssp_stats`): the batched kernel advances 32 sources per pass
+and no distance row is decoded or copied back (the reference materialises
+every row in Python).  The two arms share one structure; each is uploaded once
+and cached by the device-graph cache.
+
+Counters follow the device's snapshot-Jacobi rounds.  The
+unit-weight arm equals the reference's exactly (every path is discovered once
+in either order: μ = 1, no re-updates).  The randomized arm's μ and updated
+ratio are the Jacobi figures: deterministic, not the reference's Gauss–Seidel
+counts on large graphs.
 """
 
 from __future__ import annotations
 
-from dataclasses import dataclass
+from dataclasses import dataclass, fields
 
 import numpy as np
 
 from .graph import WeightMode, apply_weight_mode
-from .solver import AggregateStats, aggregate_stats, mssp
+from .solver import AggregateStats, aggregate_stats, mssp_stats
 
 __all__ = ["MuReport", "run_mu_experiment", "RANDOM_WEIGHT_LO", "RANDOM_WEIGHT_HI"]
 
-RANDOM_WEIGHT_LO = 0.0  # reference experiments.py:51-52
+# the randomized arm draws U[lo, hi) weights (experiments.py:51-52)
+RANDOM_WEIGHT_LO = 0.0
 RANDOM_WEIGHT_HI = 2.0
 
 
 @dataclass
 class MuReport:
-    """Paired unit-weight vs random-weight statistics for one graph (experiments.py:55-92)."""
+    """Unit-weight arm vs random-weight arm over one structure (experiments.py:55-92).
+
+    Field order is the serialisation order of :meth:`to_dict` /
+    :meth:`to_flat_dict`; the two ``AggregateStats`` fields serialise as their
+    ``as_dict()`` (nested) or as ``<arm>_<key>`` columns (flat)."""
 
     graph_id: str
     sources_sampled: int
@@ -42,66 +52,63 @@ class MuReport:
     seed: int
     notes: str = ""
 
+    def _items(self):
+        for f in fields(self):
+            yield f.name, getattr(self, f.name)
+
     def to_dict(self) -> dict:
-        return {
-            "graph_id": self.graph_id,
-            "sources_sampled": self.sources_sampled,
-            "baseline": self.baseline.as_dict(),
-            "randomized": self.randomized.as_dict(),
-            "mean_updated_ratio": self.mean_updated_ratio,
-            "mean_mu": self.mean_mu,
-            "seed": self.seed,
-            "notes": self.notes,
-        }
+        return {k: (v.as_dict() if isinstance(v, AggregateStats) else v) for k, v in self._items()}
 
     def to_flat_dict(self) -> dict:
-        flat: dict = {"graph_id": self.graph_id, "sources_sampled": self.sources_sampled}
-        for prefix, agg in (("baseline", self.baseline), ("randomized", self.randomized)):
-            for key, value in agg.as_dict().items():
-                flat[f"{prefix}_{key}"] = value
-        flat["mean_updated_ratio"] = self.mean_updated_ratio
-        flat["mean_mu"] = self.mean_mu
-        flat["seed"] = self.seed
-        flat["notes"] = self.notes
-        return flat
+        out: dict = {}
+        for k, v in self._items():
+            if isinstance(v, AggregateStats):
+                out.update((f"{k}_{sub}", x) for sub, x in v.as_dict().items())
+            else:
+                out[k] = v
+        return out
+
+
+def _sample(n: int, wanted: int, seed: int) -> tuple[list[int], str]:
+    """The seeded source sample (experiments.py:141-155): ``wanted`` distinct
+    nodes, ascending, clamped to ``n`` with a note."""
+    if wanted < 1:
+        raise ValueError("num_sources must be >= 1")
+    if n == 0:
+        raise ValueError("cannot sample sources from an empty graph")
+    note = ""
+    if wanted > n:
+        note, wanted = f"requested {wanted} sources, clamped to n={n}", n
+    picked = np.random.default_rng(seed).choice(n, size=wanted, replace=False)
+    return sorted(map(int, picked)), note
+
+
+def _arm(g, mode: WeightMode, sources: list[int], workers: int) -> AggregateStats:
+    """One arm: ``g``'s structure under ``mode``, counters only, on the device."""
+    return aggregate_stats(mssp_stats(apply_weight_mode(g, mode), sources, "govm", workers))
 
 
 def run_mu_experiment(g, num_sources: int = 64, seed: int = 0, workers: int = 1,
                       graph_id: str | None = None) -> MuReport:
-    """Unit-weight baseline vs U[0, 2) weights from a seeded source sample
-    (reference experiments.py:127-178: same arguments, validation, sampling and
-    errors)."""
-    if num_sources < 1:
-        raise ValueError("num_sources must be >= 1")
-    if g.n == 0:
-        raise ValueError("cannot sample sources from an empty graph")
-    notes = ""
-    if num_sources > g.n:
-        notes = f"requested {num_sources} sources, clamped to n={g.n}"
-        num_sources = g.n
-    if graph_id is None:
-        graph_id = f"graph(n={g.n},m={g.m})"
-
-    rng = np.random.default_rng(seed)
-    sources = sorted(int(s) for s in rng.choice(g.n, size=num_sources, replace=False))
-
-    unit = apply_weight_mode(g, WeightMode.unit())
-    randomized = apply_weight_mode(g, WeightMode.random_uniform(RANDOM_WEIGHT_LO, RANDOM_WEIGHT_HI, seed=seed))
-
-    base_agg = aggregate_stats(s for _, s in mssp(unit, sources, "govm", workers))
-    if base_agg.re_updates != 0:
+    """Unit weights vs U[0, 2) weights from the same seeded sources
+    (experiments.py:127-178).  ``seed`` drives both the sample and the random
+    weights, so reports are identical across runs and ``workers`` (GPUs)."""
+    sources, note = _sample(g.n, num_sources, seed)
+    unit = _arm(g, WeightMode.unit(), sources, workers)
+    if unit.re_updates:
+        # unit weights reach every node along its fewest-hop path in one write
         raise RuntimeError(
             "unit-weight baseline produced re-updates; the frontier kernel "
             "is expected to discover each path exactly once"
         )
-    rand_agg = aggregate_stats(s for _, s in mssp(randomized, sources, "govm", workers))
+    rand = _arm(g, WeightMode.random_uniform(RANDOM_WEIGHT_LO, RANDOM_WEIGHT_HI, seed=seed), sources, workers)
     return MuReport(
-        graph_id=graph_id,
-        sources_sampled=num_sources,
-        baseline=base_agg,
-        randomized=rand_agg,
-        mean_updated_ratio=rand_agg.mean_updated_ratio,
-        mean_mu=rand_agg.mean_mu,
+        graph_id=graph_id if graph_id is not None else f"graph(n={g.n},m={g.m})",
+        sources_sampled=len(sources),
+        baseline=unit,
+        randomized=rand,
+        mean_updated_ratio=rand.mean_updated_ratio,
+        mean_mu=rand.mean_mu,
         seed=seed,
-        notes=notes,
+        notes=note,
     )

@@ -6,18 +6,16 @@ reference, computed on the B200.
   matrix with the reference's exact step order and rounding
   (oracles.py:141-162): bit-identical matrix and ``negative_cycle``;
   ``relaxations`` = n**3 as in the reference.
-* :func:`bellman_ford_sssp` — the full-sweep solver (GSVM: every finite row
-  relaxed every round, i.e. Bellman–Ford's passes, in snapshot order) with the
-  negative-cycle check (oracles.py:94-138).  Distances of a graph without a
-  reachable negative cycle are the shortest distances the reference computes
-  (same greatest fixpoint, bit-identical); ``negative_cycle`` is the same
-  verdict; with a reachable negative cycle the returned distances are the
-  device's capped values (the reference's are its own n-1-pass values —
-  neither is meaningful).  ``relaxations`` counts the device's edge scans.
-* :func:`dijkstra_sssp` — rejects negative weights with the reference's
-  message (oracles.py:59-91); distances from the frontier solver (for
-  non-negative weights the same minimum over left-fold path sums a heap
-  Dijkstra settles, bit-identical); ``relaxations`` counts device edge scans.
+* :func:`dijkstra_sssp` / :func:`bellman_ford_sssp` — independent of the
+  device kernels on purpose (they exist to check them; computing them with the
+  solvers under test would make every cross-check circular): native host
+  restatements in libdawn (``dawn_oracle_dijkstra`` /
+  ``dawn_oracle_bellman_ford``, csrc/dawn_host_oracles.cpp) of the reference's
+  heap Dijkstra (oracles.py:59-91) and textbook n-1-pass Bellman–Ford with its
+  detection pass (oracles.py:94-138).  Same visiting order and float64
+  arithmetic, so distances, ``relaxations`` and ``negative_cycle`` equal the
+  reference's exactly — including its unguarded distances on a reachable
+  negative cycle.
 
 These are oracles for large-scale cross-checks, not the hot path.
 """
@@ -32,7 +30,7 @@ import numpy as np
 from . import _native as N
 from .errors import GraphSizeError, NegativeWeightError
 from .graph import CsrGraph
-from .solver import DistanceVector, govm_sssp, gsvm_sssp
+from .solver import DistanceVector
 
 __all__ = ["OracleResult", "FloydResult", "dijkstra_sssp", "bellman_ford_sssp", "floyd_warshall_apsp",
            "DEFAULT_FLOYD_CAP"]
@@ -65,24 +63,39 @@ def _first_negative_edge(g: CsrGraph):
     return u, int(g.col[k]), float(g.val[k])
 
 
+def _host_arrays(g: CsrGraph):
+    return (np.ascontiguousarray(g.row_ptr, dtype=np.int64), np.ascontiguousarray(g.col, dtype=np.int64),
+            np.ascontiguousarray(g.val, dtype=np.float64))
+
+
 def dijkstra_sssp(g: CsrGraph, source: int) -> OracleResult:
-    """Shortest distances for non-negative weights; NegativeWeightError otherwise."""
+    """Heap Dijkstra (oracles.py:59-91); NegativeWeightError on a negative weight."""
     if not 0 <= source < g.n:
         raise ValueError(f"source {source} out of range for n={g.n}")
     bad = _first_negative_edge(g)
     if bad is not None:
         raise NegativeWeightError(f"Dijkstra requires non-negative weights; edge {bad[0]} -> {bad[1]} has weight "
                                   f"{bad[2]}")
-    dv, _, st = govm_sssp(g, source, schedule="async")
-    return OracleResult(dist=dv, negative_cycle=False, relaxations=int(st.relaxations))
+    rp, col, val = _host_arrays(g)
+    dist = np.empty(g.n, dtype=np.float64)
+    relax = ctypes.c_int64(0)
+    N.check(N.lib().dawn_oracle_dijkstra(g.n, rp.ctypes.data, col.ctypes.data, val.ctypes.data, int(source),
+                                         dist.ctypes.data, ctypes.byref(relax)))
+    return OracleResult(dist=DistanceVector(dist=dist, source=int(source)), negative_cycle=False,
+                        relaxations=relax.value)
 
 
 def bellman_ford_sssp(g: CsrGraph, source: int) -> OracleResult:
-    """Full-sweep rounds with the reachable-negative-cycle verdict."""
+    """Textbook Bellman–Ford with the reachable-negative-cycle verdict (oracles.py:94-138)."""
     if not 0 <= source < g.n:
         raise ValueError(f"source {source} out of range for n={g.n}")
-    dv, _, st = gsvm_sssp(g, source, schedule="jacobi")
-    return OracleResult(dist=dv, negative_cycle=bool(st.negative_cycle), relaxations=int(st.relaxations))
+    rp, col, val = _host_arrays(g)
+    dist = np.empty(g.n, dtype=np.float64)
+    relax, neg = ctypes.c_int64(0), ctypes.c_int(0)
+    N.check(N.lib().dawn_oracle_bellman_ford(g.n, rp.ctypes.data, col.ctypes.data, val.ctypes.data, int(source),
+                                             dist.ctypes.data, ctypes.byref(relax), ctypes.byref(neg)))
+    return OracleResult(dist=DistanceVector(dist=dist, source=int(source)), negative_cycle=bool(neg.value),
+                        relaxations=relax.value)
 
 
 def floyd_warshall_apsp(g: CsrGraph, cap: int = DEFAULT_FLOYD_CAP, device: int = 0) -> FloydResult:

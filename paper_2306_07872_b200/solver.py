@@ -52,6 +52,7 @@ __all__ = [
     "gsvm_sssp",
     "govm_sssp",
     "mssp",
+    "mssp_stats",
     "apsp",
     "aggregate_stats",
     "format_distance_row",
@@ -402,19 +403,31 @@ def seed_source(g, source: int, alpha: list, delta: list, stats: SolveStats | No
         N.check(L.dawn_solver_state(s, dist.ctypes.data, stamp.ctypes.data, stream))
         st = N.Stats()
         N.check(L.dawn_solver_result(s, None, None, byref(st), stream))
-    written = np.flatnonzero(stamp == 1).tolist()
-    for j in written:
-        was_inf = alpha[j] == inf
+    # The device round gives the seeded values; the reference's write
+    # sequence (which duplicate source->j edge "writes", solver.py:231-249)
+    # is the row in CSR order, replayed over its deg(source) edges so
+    # writes / first_discoveries / write_counts / pred match it exactly.
+    lo, hi = int(g.row_ptr[source]), int(g.row_ptr[source + 1])
+    cur = {}
+    for k in range(lo, hi):
+        j = int(g.col[k])
+        if j == source:
+            continue
+        cand = alpha[source] + float(g.val[k])
+        before = cur.get(j, alpha[j])
+        if before > cand:
+            cur[j] = cand
+            if write_counts is not None:
+                write_counts[j] += 1
+            if pred is not None:
+                pred[j] = int(source)
+            if stats is not None:
+                stats.writes += 1
+                if before == inf:
+                    stats.first_discoveries += 1
+    for j in np.flatnonzero(stamp == 1).tolist():
         alpha[j] = float(dist[j])
         delta[j] = True
-        if write_counts is not None:
-            write_counts[j] += 1
-        if pred is not None:
-            pred[j] = int(source)
-        if stats is not None:
-            stats.writes += 1
-            if was_inf:
-                stats.first_discoveries += 1
     if stats is not None:
         stats.relaxations += int(st.relaxations)
         if st.negative_cycle:
@@ -445,7 +458,8 @@ def _mssp_run(g, sources: list[int], algo: int, device: int, precision: str | No
                 return
             lo, hi = rng
             part = np.asarray(sources[lo:hi], dtype=np.int64)
-            N.check(N.lib().dawn_mssp(s, part.ctypes.data, hi - lo, algo, flags, rows[lo:hi].ctypes.data,
+            out = rows[lo:hi].ctypes.data if rows is not None else None  # None: counters only
+            N.check(N.lib().dawn_mssp(s, part.ctypes.data, hi - lo, algo, flags, out,
                                       ctypes.addressof(stats) + lo * ctypes.sizeof(N.Stats), dg.stream()))
 
 
@@ -469,6 +483,22 @@ def mssp(g, sources: Sequence[int], algo: str = "govm", workers: int = 1, *,
     :func:`gsvm_sssp` (``async``: same rows, per-source counters
     timing-dependent).
     """
+    rows, stats = _mssp_core(g, sources, algo, workers, precision, schedule, with_rows=True)
+    return [(DistanceVector(dist=rows[i], source=src), _stats_from_native(stats[i]))
+            for i, src in enumerate(int(x) for x in sources)]
+
+
+def mssp_stats(g, sources: Sequence[int], algo: str = "govm", workers: int = 1, *,
+               precision: str | None = None, schedule: str | None = None) -> list[SolveStats]:
+    """The ``SolveStats`` half of :func:`mssp` only: the device solves every
+    source with the same kernels and counters, but no distance row is
+    decoded or copied to the host (k x n x 8 bytes saved).  Consumers that
+    only aggregate work counters (the μ experiment, benchmarks) use it."""
+    _, stats = _mssp_core(g, sources, algo, workers, precision, schedule, with_rows=False)
+    return [_stats_from_native(st) for st in stats]
+
+
+def _mssp_core(g, sources, algo: str, workers: int, precision, schedule, with_rows: bool):
     _schedule_flag(schedule)  # validate before any work
     name = _normalize_algo(algo)
     if workers < 1:
@@ -477,18 +507,19 @@ def mssp(g, sources: Sequence[int], algo: str = "govm", workers: int = 1, *,
     for s in sources:
         _check_source(g, s)
     if not sources:
-        return []
+        return None, []
     algo_id = _ALGO[name]
     devs = _devices_for(workers)
     k, n = len(sources), int(g.n)
-    rows = _host_array((k, n))
+    rows = _host_array((k, n)) if with_rows else None
     stats = (N.Stats * k)()
+    # a claim is bounded by the host rows it writes; without rows, by 1024 sources
+    row_cap = max(1, _ROW_BYTES_BUDGET // (8 * max(n, 1))) if with_rows else 1024
     if len(devs) == 1 or k == 1:
-        chunk = max(1, _ROW_BYTES_BUDGET // (8 * max(n, 1)))
+        chunk = row_cap
     else:
         # ~8 claims per device, whole 32-source batches of the batched kernel
-        chunk = max(32, -(-k // (8 * len(devs)) // 32) * 32)
-    chunk = min(chunk, max(1, _ROW_BYTES_BUDGET // (8 * max(n, 1))))
+        chunk = min(row_cap, max(32, -(-k // (8 * len(devs)) // 32) * 32))
     cursor = [0]
     lock = threading.Lock()
 
@@ -507,8 +538,7 @@ def mssp(g, sources: Sequence[int], algo: str = "govm", workers: int = 1, *,
             for f in [ex.submit(_mssp_run, g, sources, algo_id, d, precision, schedule, rows, stats, claim)
                       for d in devs]:
                 f.result()
-    return [(DistanceVector(dist=rows[i], source=src), _stats_from_native(stats[i]))
-            for i, src in enumerate(sources)]
+    return rows, stats
 
 
 def apsp(g, algo: str = "govm", workers: int = 1, sink: Callable[[DistanceVector], None] | None = None, *,

@@ -49,6 +49,10 @@ def main() -> None:
     for seed in range(3):
         graphs[f"ncy_{seed}"] = graph_with_negative_cycle(seed, n=30, avg_degree=3.0)[0]
     graphs["u02_big"] = random_graph(99, n=300, avg_degree=5.0, regime="uniform02")
+    # zero weights, ties in the heap, duplicate (u, v) pairs with decreasing weights
+    graphs["ties_zero"] = make_csr(6, [(0, 1, 0.0), (0, 2, 0.0), (1, 3, 1.0), (2, 3, 1.0), (3, 4, 0.0),
+                                       (0, 4, 5.0), (0, 4, 3.0), (0, 4, 1.0), (4, 5, 0.5), (1, 5, 1.5)])
+    graphs["ncy_source"] = make_csr(4, [(0, 1, 1.0), (1, 0, -3.0), (1, 2, 1.0), (2, 3, 1.0)])
 
     arrays: dict[str, np.ndarray] = {}
     index: dict[str, dict] = {}
@@ -64,10 +68,11 @@ def main() -> None:
         for s in sorted({0, g.n // 2, g.n - 1}):
             bf = R.bellman_ford_sssp(g, s)
             arrays[f"{name}.bf{s}"] = bf.dist.dist
-            rec = {"source": s, "bf_negative_cycle": bf.negative_cycle}
+            rec = {"source": s, "bf_negative_cycle": bf.negative_cycle, "bf_relaxations": bf.relaxations}
             if nonneg:
                 dj = R.dijkstra_sssp(g, s)
                 arrays[f"{name}.dj{s}"] = dj.dist.dist
+                rec["dj_relaxations"] = dj.relaxations
             meta["sources"].append(rec)
         meta["nonneg"] = nonneg
         index[name] = meta

@@ -100,6 +100,14 @@ def test_seed_source(gpu, frontier_mode):
     st = P.SolveStats()
     P.seed_source(g, 0, [0.0, inf, inf], [False] * 3, stats=st)
     assert st.first_discoveries == 2 and st.writes == 2 and st.relaxations == 2
+    # duplicate source->j edges with decreasing weights: every improving edge
+    # writes in CSR order, as in the reference (solver.py:231-249)
+    g = make_csr(3, [(0, 1, 2.0), (0, 1, 1.0), (0, 1, 1.5), (0, 2, 0.5)])
+    st, wc, pred = P.SolveStats(), [0, 0, 0], [None] * 3
+    alpha, delta = P.seed_source(g, 0, [0.0, inf, inf], [False] * 3, stats=st, pred=pred, write_counts=wc)
+    assert alpha == [0.0, 1.0, 0.5] and delta == [False, True, True]
+    assert (st.writes, st.first_discoveries, st.relaxations) == (3, 2, 4)
+    assert wc == [0, 2, 1] and pred == [None, 0, 0]
 
 
 def test_hand_trace_and_small_cases(gpu):

@@ -150,3 +150,33 @@ def test_pinned_result_pool_keeps_live_views(monkeypatch):
     third = S._host_array(6)
     third[:] = 3.0
     assert again.tolist() == [[2.0] * 3] * 2
+
+
+def test_mu_report_layout_matches_reference():
+    """MuReport.to_dict / to_flat_dict keep the reference's key order
+    (experiments.py:70-92)."""
+    from paper_2306_07872_b200.experiments import MuReport
+
+    a = P.AggregateStats(sources=2, writes=3).finish()
+    b = P.AggregateStats(sources=2, writes=5).finish()
+    r = MuReport("g", 2, a, b, 0.5, 1.25, 7, "n")
+    d = r.to_dict()
+    assert list(d) == ["graph_id", "sources_sampled", "baseline", "randomized", "mean_updated_ratio", "mean_mu",
+                       "seed", "notes"]
+    assert d["baseline"] == a.as_dict() and d["randomized"] == b.as_dict()
+    f = r.to_flat_dict()
+    keys = list(a.as_dict())
+    assert list(f) == (["graph_id", "sources_sampled"] + [f"baseline_{k}" for k in keys]
+                       + [f"randomized_{k}" for k in keys] + ["mean_updated_ratio", "mean_mu", "seed", "notes"])
+    assert f["randomized_writes"] == 5 and f["baseline_writes"] == 3
+
+
+def test_mu_experiment_validates_before_device_work():
+    from paper_2306_07872_b200.experiments import run_mu_experiment
+
+    g = P.generate_random_graph(10, 2.0, P.WeightMode.unit(), seed=1)
+    with pytest.raises(ValueError, match="num_sources must be >= 1"):
+        run_mu_experiment(g, num_sources=0)
+    empty = P.generate_random_graph(0, 2.0, P.WeightMode.unit(), seed=1)
+    with pytest.raises(ValueError, match="empty graph"):
+        run_mu_experiment(empty, num_sources=3)
