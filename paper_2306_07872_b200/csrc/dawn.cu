@@ -29,6 +29,7 @@
 #include "dawn_batch.cuh"
 #include "dawn_csr.cuh"
 #include "dawn_fw.cuh"
+#include "dawn_nearfar.cuh"
 
 using namespace dawn;
 
@@ -183,6 +184,13 @@ struct dawn_solver_s {
   bool wide = false;
   int fb_pref = -1;                   // tunable "bitmap_frontier": -1 auto, 0 off, 1 on
   bool fb = false;
+  int nf_pref = -1;                   // tunable "nearfar": -1 auto (low-degree graphs), 0 off, 1 on
+  bool nf = false;                    // async solves without negative weights run dawn_nearfar
+  double nf_delta = 0;                // tunable "nearfar_delta": bucket width in weight units (0 = auto)
+  double nf_delta_mean = 8;           // tunable "nearfar_delta_mean": auto width = this * mean edge weight
+  double mean_w = -1;                 // mean edge weight (computed on first near-far solve)
+  double nf_cap = 64;                 // tunable "nearfar_batches": continuation batches per warp per round
+  int nf_grid = 1;
   double batch_min_sources = 4;       // tunable: dawn_mssp batches when k >= this
   double batch_sparse_util = 4;       // tunable: batched rounds averaging < this active sources per edge go lane-sparse
   int ebits = 32;
@@ -616,6 +624,9 @@ struct Impl {
     P.wl_ring = s->worklist_edges > 0 ? s->wl_ring : nullptr;
     P.wl_mask = s->wl_cap ? s->wl_cap - 1 : 0;
     P.wl_edges = (unsigned long long)s->worklist_edges;
+    P.nf_delta = s->nf_delta > 0 ? s->nf_delta : s->nf_delta_mean * std::max(s->mean_w, 0.0);
+    if (!(P.nf_delta > 0)) P.nf_delta = std::is_floating_point<V>::value ? 1e-3 : 1.0;
+    P.nf_cap = (uint32_t)std::min(s->nf_cap, 4.0e9);
     return P;
   }
 
@@ -633,6 +644,25 @@ struct Impl {
       return raw ? (void*)dawn_persistent<V, EI, false, true, XI_NARROW, true>
                  : (void*)dawn_persistent<V, EI, false, false, XI_NARROW, true>;
     return s->wide ? kernel<XW>(pred, raw) : kernel<XI_NARROW>(pred, raw);
+  }
+
+  // mean edge weight (the near-far bucket width is a multiple of it); once per solver
+  static int mean_weight(dawn_solver_t s, cudaStream_t stream) {
+    const int64_t m = s->g->m;
+    double* d = nullptr;
+    CK(dmalloc(&d, sizeof(double)));
+    CK(cudaMemsetAsync(d, 0, sizeof(double), stream));
+    if (m > 0) {
+      const int blocks = (int)std::min<int64_t>(148 * 4, (m + 255) / 256);
+      dawn_weight_sum<V><<<blocks, 256, 0, stream>>>(s->g->e2, s->g->ew, (uint64_t)m, d);
+      CK(cudaGetLastError());
+    }
+    double h = 0;
+    CK(cudaMemcpyAsync(&h, d, sizeof(double), cudaMemcpyDeviceToHost, stream));
+    CK(cudaStreamSynchronize(stream));
+    dfree(d);
+    s->mean_w = m > 0 ? h / (double)m : 0.0;
+    return DAWN_OK;
   }
 
   static int setup(dawn_solver_t s) {
@@ -675,6 +705,14 @@ struct Impl {
     int bpw = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpw, dawn_worklist<V, EI>, NT, 0));
     s->wl_grid = std::max(1, bpw) * nsm;
+    // near-far schedule (async, no negative weights): on by default where the bitmap frontier is
+    s->nf = s->nf_pref < 0 ? s->fb : s->nf_pref > 0;
+    int bpn = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpn, dawn_nearfar<V, EI>, NT, 0));
+    if (bpn < 1) return fail(DAWN_ECUDA, "near-far kernel cannot be resident");
+    const int64_t chunks = ((n + 31) / 32 + 127) / 128;  // 128-word sweep chunks, one per warp
+    s->nf_grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)std::min(bpn, DAWN_MIN_BLOCKS) * nsm,
+                                                            (chunks + WPB - 1) / WPB));
     return DAWN_OK;
   }
 
@@ -690,7 +728,19 @@ struct Impl {
     return DAWN_OK;
   }
 
+  static bool nearfar_eligible(dawn_solver_t s, unsigned max_rounds) {
+    return s->nf && (s->run_flags & DAWN_F_ASYNC) && !(s->run_flags & DAWN_F_PRED) && s->algo == DAWN_GOVM &&
+           max_rounds == 0xFFFFFFFFu && !s->g->has_negative;
+  }
+
   static int run(dawn_solver_t s, unsigned max_rounds, cudaStream_t stream) {
+    if (nearfar_eligible(s, max_rounds)) {
+      if (s->mean_w < 0) TRY(mean_weight(s, stream));
+      KParams<V, EI> P = params(s, max_rounds);
+      void* args[] = {&P};
+      CK(cudaLaunchCooperativeKernel((void*)dawn_nearfar<V, EI>, dim3(s->nf_grid), dim3(NT), args, 0, stream));
+      return DAWN_OK;
+    }
     KParams<V, EI> P = params(s, max_rounds);
     void* args[] = {&P};
     void* fn = kernel_for(s, P.pred_on != 0);
@@ -984,6 +1034,27 @@ extern "C" int dawn_solver_tune(dawn_solver_t s, const char* key, double value) 
     s->fb_pref = (int)value;
     CK(cudaSetDevice(s->g->device));
     return DISPATCH(s->g, setup(s));
+  }
+  if (!strcmp(key, "nearfar")) {
+    if (!(value == -1.0 || value == 0.0 || value == 1.0)) return fail(DAWN_EINVAL, "nearfar must be -1, 0 or 1");
+    s->nf_pref = (int)value;
+    CK(cudaSetDevice(s->g->device));
+    return DISPATCH(s->g, setup(s));
+  }
+  if (!strcmp(key, "nearfar_delta")) {
+    if (!(value >= 0.0)) return fail(DAWN_EINVAL, "nearfar_delta must be >= 0");
+    s->nf_delta = value;
+    return DAWN_OK;
+  }
+  if (!strcmp(key, "nearfar_batches")) {
+    if (!(value >= 0.0)) return fail(DAWN_EINVAL, "nearfar_batches must be >= 0");
+    s->nf_cap = value;
+    return DAWN_OK;
+  }
+  if (!strcmp(key, "nearfar_delta_mean")) {
+    if (!(value > 0.0)) return fail(DAWN_EINVAL, "nearfar_delta_mean must be > 0");
+    s->nf_delta_mean = value;
+    return DAWN_OK;
   }
   if (!strcmp(key, "batch_sparse_util")) {
     if (!(value >= 0.0 && value <= 33.0)) return fail(DAWN_EINVAL, "batch_sparse_util must be in [0, 33]");

@@ -290,6 +290,10 @@ struct DevState {
   unsigned long long wl_items;              // items taken (statistics)
   unsigned wl_mode;                         // the persistent kernel handed the solve to dawn_worklist
   unsigned long long wl_batches, wl_busy_ns, wl_wait_ns, wl_t0, wl_t1;  // worklist timeline (sums over warps)
+  // near-far schedule (dawn_nearfar): per-round counters, triple-buffered by round
+  unsigned long long nf_near[3];    // near rows left for the next round (ring overflow)
+  unsigned long long nf_farmin[3];  // smallest key among the far rows left pending (all-ones = none)
+  unsigned long long nf_buckets;    // threshold advances (statistics)
 };
 
 }  // namespace dawn

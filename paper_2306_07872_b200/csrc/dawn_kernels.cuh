@@ -72,6 +72,8 @@ struct KParams {
   unsigned long long* wl_ring;         // ring of 16-byte row items (uint4); nullptr = off
   unsigned long long wl_mask;          // ring capacity - 1 (power of two)
   unsigned long long wl_edges;
+  double nf_delta;                     // near-far schedule: bucket width in weight units (dawn_nearfar.cuh)
+  uint32_t nf_cap;                     // near-far: continuation batches a warp may run per round
 };
 
 constexpr int WPB = NT / 32;       // warps per CTA
