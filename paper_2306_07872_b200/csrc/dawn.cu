@@ -200,12 +200,12 @@ struct dawn_solver_s {
   bool last_batch = false;       // the last solve on this solver was a batch (round profile source)
   void* bd = nullptr;            // K[n][32]
   uint32_t* bmask[4] = {nullptr, nullptr, nullptr, nullptr};  // nmask, w1, w2, smask
-  uint32_t* bqnode = nullptr;
-  uint32_t* bqmask = nullptr;
-  void* bqoff = nullptr;
-  void* bqbase = nullptr;
+  uint32_t* bqnode[2] = {nullptr, nullptr};  // row lists 0 (whole line) and 1 (lane by lane)
+  uint32_t* bqmask[2] = {nullptr, nullptr};
+  void* bqoff[2] = {nullptr, nullptr};
+  void* bqbase[2] = {nullptr, nullptr};
   void* bqkey = nullptr;         // K[n][32]
-  uint32_t* btile = nullptr;
+  uint32_t* btile[2] = {nullptr, nullptr};
   BState* bst = nullptr;
   BState* bst_host = nullptr;    // pinned, one per batch in flight
   int64_t bst_host_cap = 0;
@@ -785,12 +785,14 @@ struct Impl {
     const size_t ks = sizeof(K), es = sizeof(EI);
     CK(dmalloc(&s->bd, ks * BL * (size_t)n));
     for (int i = 0; i < 4; ++i) CK(dmalloc(&s->bmask[i], 4 * (size_t)n));
-    CK(dmalloc(&s->bqnode, 4 * (size_t)n));
-    CK(dmalloc(&s->bqmask, 4 * (size_t)n));
-    CK(dmalloc(&s->bqoff, es * (size_t)n));
-    CK(dmalloc(&s->bqbase, es * (size_t)n));
+    for (int q = 0; q < 2; ++q) {
+      CK(dmalloc(&s->bqnode[q], 4 * (size_t)n));
+      CK(dmalloc(&s->bqmask[q], 4 * (size_t)n));
+      CK(dmalloc(&s->bqoff[q], es * (size_t)n));
+      CK(dmalloc(&s->bqbase[q], es * (size_t)n));
+      CK(dmalloc(&s->btile[q], 4 * (size_t)(m / BWT + 4)));
+    }
     CK(dmalloc(&s->bqkey, ks * BL * (size_t)n));
-    CK(dmalloc(&s->btile, 4 * (size_t)(m / BWT + 4)));
     CK(dmalloc(&s->bst, sizeof(BState)));
     CK(cudaMemset(s->bst, 0, sizeof(BState)));
     CK(cudaMemset(s->bmask[0], 0, 4 * (size_t)n));
@@ -834,12 +836,14 @@ struct Impl {
     P.w1 = s->bmask[1];
     P.w2 = s->bmask[2];
     P.smask = s->bmask[3];
-    P.qnode = s->bqnode;
-    P.qmask = s->bqmask;
-    P.qoff = (EI*)s->bqoff;
-    P.qbase = (EI*)s->bqbase;
+    for (int q = 0; q < 2; ++q) {
+      P.qnode[q] = s->bqnode[q];
+      P.qmask[q] = s->bqmask[q];
+      P.qoff[q] = (EI*)s->bqoff[q];
+      P.qbase[q] = (EI*)s->bqbase[q];
+      P.tile_row[q] = s->btile[q];
+    }
     P.qkey = (K*)s->bqkey;
-    P.tile_row = s->btile;
     P.st = s->bst;
     for (int l = 0; l < BL; ++l) P.src[l] = l < nl ? (uint32_t)src[l] : 0xFFFFFFFFu;
     P.ebits = s->ebits;
@@ -979,12 +983,14 @@ static void solver_free(dawn_solver_t s) {
   dfree(s->cta_prof);
   dfree(s->bd);
   for (int i = 0; i < 4; ++i) dfree(s->bmask[i]);
-  dfree(s->bqnode);
-  dfree(s->bqmask);
-  dfree(s->bqoff);
-  dfree(s->bqbase);
+  for (int q = 0; q < 2; ++q) {
+    dfree(s->bqnode[q]);
+    dfree(s->bqmask[q]);
+    dfree(s->bqoff[q]);
+    dfree(s->bqbase[q]);
+    dfree(s->btile[q]);
+  }
   dfree(s->bqkey);
-  dfree(s->btile);
   dfree(s->bst);
   hfree(s->bst_host);
   dfree(s->bout);

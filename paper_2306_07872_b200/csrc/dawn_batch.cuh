@@ -44,6 +44,7 @@ constexpr int BWT = 32;   // virtual edges per warp tile (<= 32 rows per tile)
 
 struct BState {
   unsigned long long res[2];   // packed frontier reservation (count << ebits | edges), by round parity
+  unsigned long long res_s[2]; // ... of the lane-sparse row list (async schedule), by round parity
   unsigned long long le[2];    // lane-edges (relaxations) of the round with this parity
   unsigned bar;                // grid barrier word (never reset)
   unsigned wrote[2];           // lanes that lowered any node in the round with this parity
@@ -67,17 +68,20 @@ struct BParams {
   uint32_t* w1;                    // [n] lanes that lowered it in >= 1 round
   uint32_t* w2;                    // [n] ... in >= 2 rounds
   uint32_t* smask;                 // [n] lanes whose source is the node (GSVM frontier)
-  uint32_t* qnode;
-  uint32_t* qmask;
-  EI* qoff;
-  EI* qbase;
-  K* qkey;                         // [cap][32] snapshot of the frontier rows
-  uint32_t* tile_row;
+  // frontier row lists: [0] = rows relaxed across the whole distance line,
+  // [1] = rows with few active sources, relaxed lane by lane (async schedule)
+  uint32_t* qnode[2];
+  uint32_t* qmask[2];
+  EI* qoff[2];
+  EI* qbase[2];
+  K* qkey;                         // [cap][32] snapshot of the frontier rows (list 0)
+  uint32_t* tile_row[2];
   BState* st;
   uint32_t src[BL];                // lane -> source node (0xFFFFFFFF = unused lane)
   int ebits;
   int algo;                        // 0 = GOVM, 1 = GSVM
-  uint32_t sparse_util;            // a round with lane-edges < this * edges relaxes lane-sparse
+  uint32_t sparse_util;            // a round with lane-edges < this * edges relaxes lane-sparse;
+                                   // async: rows with fewer active sources go to list 1
   unsigned long long* prof;        // optional per-round timeline, 4 words/round, or nullptr
   unsigned prof_cap;
 };
@@ -85,7 +89,7 @@ struct BParams {
 template <class V, class EI>
 struct __align__(16) BSmem {
   unsigned long long scr64[NT / 32];
-  unsigned long long basepk;
+  unsigned long long basepk, basepk_s;
   unsigned rl[BL];            // relaxations per source lane counted by lane-sparse rounds (< 2^32 per CTA)
   uint32_t src[BL];           // lane -> source node (lane-sparse source guard)
 };
@@ -236,9 +240,9 @@ __device__ void bphase_build(const BParams<V, EI>& P, uint32_t r, uint32_t activ
 #pragma unroll
     for (int j = 0; j < ITEMS; ++j) anyF |= F[j];
     EI rp[ITEMS + 1];
-    unsigned sel = 0;
-    uint32_t mycnt = 0;
-    EI mydeg = 0;
+    unsigned sel = 0, sel_s = 0;  // rows of list 0 / list 1 (few active sources, async)
+    uint32_t mycnt = 0, mycnt_s = 0;
+    EI mydeg = 0, mydeg_s = 0;
     if (anyF) {
       if (full) {
         ldg8<EI>(P.row_ptr + u0, *reinterpret_cast<EI(*)[ITEMS]>(rp));
@@ -251,9 +255,15 @@ __device__ void bphase_build(const BParams<V, EI>& P, uint32_t r, uint32_t activ
 #pragma unroll
       for (int j = 0; j < ITEMS; ++j) {
         if (F[j] && u0 + j < n && rp[j + 1] > rp[j]) {
-          sel |= 1u << j;
-          mycnt++;
-          mydeg += rp[j + 1] - rp[j];
+          if (LIVE && (uint32_t)__popc(F[j]) < P.sparse_util) {
+            sel_s |= 1u << j;
+            mycnt_s++;
+            mydeg_s += rp[j + 1] - rp[j];
+          } else {
+            sel |= 1u << j;
+            mycnt++;
+            mydeg += rp[j + 1] - rp[j];
+          }
         }
       }
     }
@@ -261,62 +271,72 @@ __device__ void bphase_build(const BParams<V, EI>& P, uint32_t r, uint32_t activ
     unsigned long long tot;
     const unsigned long long incl = block_incl_sum<unsigned long long>(mine, s.scr64, &tot);
     if (threadIdx.x == 0 && tot != 0ull) s.basepk = atomicAdd(&P.st->res[r & 1], tot);
+    unsigned long long mine_s = 0, incl_s = 0;
+    if (LIVE) {
+      __syncthreads();  // scr64 reuse
+      mine_s = ((unsigned long long)mycnt_s << eb) | (unsigned long long)mydeg_s;
+      unsigned long long tot_s;
+      incl_s = block_incl_sum<unsigned long long>(mine_s, s.scr64, &tot_s);
+      if (threadIdx.x == 0 && tot_s != 0ull) s.basepk_s = atomicAdd(&P.st->res_s[r & 1], tot_s);
+    }
     __syncthreads();
-    if (!__any_sync(0xffffffffu, sel != 0u)) continue;
+    if (!__any_sync(0xffffffffu, (sel | sel_s) != 0u)) continue;
     {  // lane-edges of round r: chooses the relax mode of the X phase (and the profile)
       unsigned long long le = 0;
 #pragma unroll
       for (int j = 0; j < ITEMS; ++j)
-        if ((sel >> j) & 1u) le += (unsigned long long)__popc(F[j]) * (unsigned long long)(rp[j + 1] - rp[j]);
+        if (((sel | sel_s) >> j) & 1u) le += (unsigned long long)__popc(F[j]) * (unsigned long long)(rp[j + 1] - rp[j]);
       le = warp_sum_u64(le);
       if (lane == 0 && le) {
         atomicAdd(&P.st->le[r & 1], le);
         if (P.prof != nullptr && r < P.prof_cap) atomicAdd(P.prof + 4 * r + 3, le);
       }
     }
-    if (!sel) continue;
     // this thread's entries: metadata, tile marks and the 32-lane snapshot
     // (one full 128/256-byte line per entry, vector loads all in flight)
-    const unsigned long long at = s.basepk + incl - mine;
-    uint32_t pos = (uint32_t)pk_count(at, eb);
-    EI off = (EI)pk_edges(at, eb);
-    constexpr int NV = BL * (int)sizeof(K) / 16;
+#pragma unroll 1
+    for (int q = 0; q < (LIVE ? 2 : 1); ++q) {
+      const unsigned qs = q ? sel_s : sel;
+      if (!qs) continue;
+      const unsigned long long at = q ? s.basepk_s + incl_s - mine_s : s.basepk + incl - mine;
+      uint32_t pos = (uint32_t)pk_count(at, eb);
+      EI off = (EI)pk_edges(at, eb);
+      constexpr int NV = BL * (int)sizeof(K) / 16;
 #pragma unroll
-    for (int j = 0; j < ITEMS; ++j) {
-      if ((sel >> j) & 1u) {
-        const uint32_t v = u0 + j;
-        const EI dg = rp[j + 1] - rp[j];
-        const uint4* srcl = reinterpret_cast<const uint4*>(P.bd + (size_t)v * BL);
-        uint4* dstl = reinterpret_cast<uint4*>(P.qkey + (size_t)pos * BL);
-        uint4 x[8];
-        if (!LIVE) {
+      for (int j = 0; j < ITEMS; ++j) {
+        if ((qs >> j) & 1u) {
+          const uint32_t v = u0 + j;
+          const EI dg = rp[j + 1] - rp[j];
+          const uint4* srcl = reinterpret_cast<const uint4*>(P.bd + (size_t)v * BL);
+          uint4* dstl = reinterpret_cast<uint4*>(P.qkey + (size_t)pos * BL);
+          uint4 x[8];
+          if (!LIVE) {
 #pragma unroll
-          for (int q = 0; q < 8; ++q) x[q] = __ldcg(srcl + q);
-        }
-        P.qnode[pos] = v;
-        P.qmask[pos] = F[j];
-        P.qoff[pos] = off;
-        P.qbase[pos] = rp[j] - off;
-        {
-          const EI t0 = (off + (EI)(BWT - 1)) / (EI)BWT;
-          const EI t1 = (off + dg - 1) / (EI)BWT;
-          for (EI tt = t0; tt <= t1; ++tt) P.tile_row[tt] = pos;
-        }
-        if (!LIVE) {  // the async schedule reads the live line instead
-#pragma unroll
-          for (int q = 0; q < 8; ++q) dstl[q] = x[q];
-        }
-        if (!LIVE) {
-#pragma unroll
-          for (int h = 8; h < NV; h += 8) {  // 8-byte keys: second half of the line
-#pragma unroll
-            for (int q = 0; q < 8; ++q) x[q] = __ldcg(srcl + h + q);
-#pragma unroll
-            for (int q = 0; q < 8; ++q) dstl[h + q] = x[q];
+            for (int qq = 0; qq < 8; ++qq) x[qq] = __ldcg(srcl + qq);
           }
+          P.qnode[q][pos] = v;
+          P.qmask[q][pos] = F[j];
+          P.qoff[q][pos] = off;
+          P.qbase[q][pos] = rp[j] - off;
+          {
+            const EI t0 = (off + (EI)(BWT - 1)) / (EI)BWT;
+            const EI t1 = (off + dg - 1) / (EI)BWT;
+            for (EI tt = t0; tt <= t1; ++tt) P.tile_row[q][tt] = pos;
+          }
+          if (!LIVE) {  // the async schedule reads the live line instead
+#pragma unroll
+            for (int qq = 0; qq < 8; ++qq) dstl[qq] = x[qq];
+#pragma unroll
+            for (int h = 8; h < NV; h += 8) {  // 8-byte keys: second half of the line
+#pragma unroll
+              for (int qq = 0; qq < 8; ++qq) x[qq] = __ldcg(srcl + h + qq);
+#pragma unroll
+              for (int qq = 0; qq < 8; ++qq) dstl[h + qq] = x[qq];
+            }
+          }
+          pos++;
+          off += dg;
         }
-        pos++;
-        off += dg;
       }
     }
   }
@@ -372,19 +392,19 @@ struct BRows {        // row metadata of a tile in flight
 };
 
 template <class V, class EI, bool LIVE>
-__device__ __forceinline__ void brows_load(const BParams<V, EI>& P, EI t, EI T, uint32_t cnt, uint32_t lane,
+__device__ __forceinline__ void brows_load(const BParams<V, EI>& P, int q, EI t, EI T, uint32_t cnt, uint32_t lane,
                                            BRows<V, EI>& R) {
-  R.i0 = __ldca(P.tile_row + t);
-  R.il = (t + 1 < T) ? __ldca(P.tile_row + t + 1) : cnt - 1;
+  R.i0 = __ldca(P.tile_row[q] + t);
+  R.il = (t + 1 < T) ? __ldca(P.tile_row[q] + t + 1) : cnt - 1;
   R.off = 0;
   R.base = 0;
   R.rmask = 0;
   R.rnode = 0;
   if (lane <= R.il - R.i0) {
-    R.off = __ldca(P.qoff + R.i0 + lane);
-    R.base = __ldca(P.qbase + R.i0 + lane);
-    R.rmask = __ldca(P.qmask + R.i0 + lane);
-    if (LIVE) R.rnode = __ldca(P.qnode + R.i0 + lane);
+    R.off = __ldca(P.qoff[q] + R.i0 + lane);
+    R.base = __ldca(P.qbase[q] + R.i0 + lane);
+    R.rmask = __ldca(P.qmask[q] + R.i0 + lane);
+    if (LIVE) R.rnode = __ldca(P.qnode[q] + R.i0 + lane);
   }
 }
 
@@ -413,7 +433,7 @@ __device__ __forceinline__ void btile_issue(const BParams<V, EI>& P, EI t, EI E,
 // thread owns one edge and walks the row's set lanes one by one (scalar
 // gathers), instead of 8 threads covering all 32 lanes of the distance line.
 template <class V, class EI, bool SPARSE, bool LIVE>
-__device__ void bphase_expand(const BParams<V, EI>& P, uint32_t r, const uint32_t (&msrc)[BLanes<V>::LPT],
+__device__ void bphase_expand(const BParams<V, EI>& P, int q, uint32_t r, const uint32_t (&msrc)[BLanes<V>::LPT],
                               unsigned& guard, unsigned& wrote, unsigned long long (&accR)[BLanes<V>::LPT],
                               BSmem<V, EI>& sm) {
   using CD = Codec<V, true>;
@@ -431,7 +451,7 @@ __device__ void bphase_expand(const BParams<V, EI>& P, uint32_t r, const uint32_
   // infinite candidate never written (solver.py:298, :373)
   constexpr K CAP = std::is_same<V, float>::value ? (K)0x7F800000u
                   : std::is_same<V, double>::value ? (K)0x7FF0000000000000ull : CD::INF;
-  const unsigned long long pk = ldcg(&P.st->res[r & 1]);
+  const unsigned long long pk = ldcg(q ? &P.st->res_s[r & 1] : &P.st->res[r & 1]);
   const uint32_t cnt = (uint32_t)pk_count(pk, P.ebits);
   const EI E = (EI)pk_edges(pk, P.ebits);
   if (E == 0) return;
@@ -448,17 +468,17 @@ __device__ void bphase_expand(const BParams<V, EI>& P, uint32_t r, const uint32_
   BRows<V, EI> Rn;
   {
     BRows<V, EI> R0;
-    brows_load<V, EI, LIVE>(P, t, T, cnt, lane, R0);
+    brows_load<V, EI, LIVE>(P, q, t, T, cnt, lane, R0);
     btile_issue<V, EI>(P, t, E, lane, R0, A);
   }
   Bt.len = 0;
   if (t + GW < T) {
     BRows<V, EI> R1;
-    brows_load<V, EI, LIVE>(P, t + GW, T, cnt, lane, R1);
+    brows_load<V, EI, LIVE>(P, q, t + GW, T, cnt, lane, R1);
     btile_issue<V, EI>(P, t + GW, E, lane, R1, Bt);
   }
   bool have_rn = t + 2 * GW < T;
-  if (have_rn) brows_load<V, EI, LIVE>(P, t + 2 * GW, T, cnt, lane, Rn);
+  if (have_rn) brows_load<V, EI, LIVE>(P, q, t + 2 * GW, T, cnt, lane, Rn);
   // relaxations (solver.py:297, :372) of this thread's lanes: LPT 8/16-bit
   // counters packed in one register (a thread sees STEPS <= 16 edges per tile),
   // flushed into accR after every tile
@@ -557,7 +577,7 @@ __device__ void bphase_expand(const BParams<V, EI>& P, uint32_t r, const uint32_
     if (have_rn) {
       btile_issue<V, EI>(P, t + GW, E, lane, Rn, Bt);
       have_rn = t + 2 * GW < T;
-      if (have_rn) brows_load<V, EI, LIVE>(P, t + 2 * GW, T, cnt, lane, Rn);
+      if (have_rn) brows_load<V, EI, LIVE>(P, q, t + 2 * GW, T, cnt, lane, Rn);
     }
   }
 }
@@ -607,6 +627,7 @@ __global__ void __launch_bounds__(NT, DAWN_BATCH_MIN_BLOCKS) dawn_batch_persiste
     if (prof) P.prof[4 * r + 0] = globaltimer();
     if (leader) {  // last read by X(r-1), next written by B(r+1)
       st->res[(r + 1) & 1] = 0ull;
+      st->res_s[(r + 1) & 1] = 0ull;
       st->le[(r + 1) & 1] = 0ull;
     }
     bphase_build<V, EI, LIVE>(P, r, active, s, accW, accFD, accMW);
@@ -622,8 +643,14 @@ __global__ void __launch_bounds__(NT, DAWN_BATCH_MIN_BLOCKS) dawn_batch_persiste
       // lane-sparse relax when the round's rows carry few active sources on average
       const unsigned long long E = pk_edges(ldcg(&st->res[r & 1]), P.ebits);
       const unsigned long long LE = ldcg(&st->le[r & 1]);
-      if (LE < (unsigned long long)P.sparse_util * E) bphase_expand<V, EI, true, LIVE>(P, r, msrc, guard, wrote, accR, s);
-      else bphase_expand<V, EI, false, LIVE>(P, r, msrc, guard, wrote, accR, s);
+      if (LIVE) {  // rows split by their active sources in the B phase
+        bphase_expand<V, EI, false, LIVE>(P, 0, r, msrc, guard, wrote, accR, s);
+        bphase_expand<V, EI, true, LIVE>(P, 1, r, msrc, guard, wrote, accR, s);
+      } else if (LE < (unsigned long long)P.sparse_util * E) {
+        bphase_expand<V, EI, true, LIVE>(P, 0, r, msrc, guard, wrote, accR, s);
+      } else {
+        bphase_expand<V, EI, false, LIVE>(P, 0, r, msrc, guard, wrote, accR, s);
+      }
     }
     wrote = __reduce_or_sync(0xffffffffu, wrote);
     if (lane == 0 && wrote) atomicOr(&st->wrote[r & 1], wrote);
@@ -683,6 +710,7 @@ __global__ void dawn_batch_init(BParams<V, EI> P) {
   if (l == 0) {
     BState* st = P.st;
     st->res[0] = st->res[1] = 0ull;
+    st->res_s[0] = st->res_s[1] = 0ull;
     st->le[0] = st->le[1] = 0ull;
     st->wrote[0] = st->wrote[1] = 0u;
     st->guard = 0u;

@@ -34,7 +34,17 @@ KEYS = [
     ("launch__block_size", "block"),
     ("smsp__inst_executed.sum", "warp instructions"),
     ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue active %"),
+    ("l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum", "global load sectors"),
+    ("l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum", "global load requests"),
+    ("l1tex__t_sectors_pipe_lsu_mem_global_op_st.sum", "global store sectors"),
+    ("l1tex__t_requests_pipe_lsu_mem_global_op_st.sum", "global store requests"),
+    ("l1tex__t_sectors_pipe_lsu_mem_global_op_atom.sum", "global atom sectors"),
+    ("l1tex__t_requests_pipe_lsu_mem_global_op_atom.sum", "global atom requests"),
+    ("l1tex__t_sectors_pipe_lsu_mem_global_op_red.sum", "global red sectors"),
+    ("l1tex__t_requests_pipe_lsu_mem_global_op_red.sum", "global red requests"),
 ]
+RATIOS = [("ld", "global loads"), ("st", "global stores"), ("atom", "global atomics (returning)"),
+          ("red", "global reductions (red.*)")]
 
 
 def launches(path: str):
@@ -75,7 +85,41 @@ def rep(path: str):
             if k in h:
                 i = h.index(k)
                 out.append(f"| {label} (`{k}`) | {row[i]} | {u[i]} |")
+        for op, label in RATIOS:
+            ks = f"l1tex__t_sectors_pipe_lsu_mem_global_op_{op}.sum"
+            kr = f"l1tex__t_requests_pipe_lsu_mem_global_op_{op}.sum"
+            if ks in h and kr in h:
+                sec = float(row[h.index(ks)].replace(",", "") or 0)
+                req = float(row[h.index(kr)].replace(",", "") or 0)
+                if req:
+                    out.append(f"| **sectors / request, {label}** | {sec / req:.2f} | sector/request |")
         out.append("")
+    return out
+
+
+def stalls(path: str, top: int = 15):
+    """Top source lines by sampled warp stalls (needs -lineinfo + --import-source on)."""
+    txt = subprocess.run(["ncu", "-i", path, "--page", "source", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(txt.splitlines()))
+    hi = next((i for i, r in enumerate(rows) if any("Warp Stall Sampling (All" in c for c in r)), None)
+    if hi is None:
+        return ["(no source page)"]
+    h = rows[hi]
+    si = next(i for i, c in enumerate(h) if "Warp Stall Sampling (All" in c)
+    li = h.index("# Address") if "# Address" in h else (h.index("Line") if "Line" in h else 0)
+    ci = h.index("Source") if "Source" in h else len(h) - 1
+    body = []
+    for r in rows[hi + 1:]:
+        if len(r) <= max(si, ci):
+            continue
+        try:
+            body.append((float(r[si].replace(",", "") or 0), r[li], r[ci].strip()[:110]))
+        except ValueError:
+            continue
+    allv = sum(b[0] for b in body) or 1.0
+    out = ["| share | line | source |", "|---:|---:|---|"]
+    for v, ln, src in sorted(body, key=lambda b: -b[0])[:top]:
+        out.append(f"| {100 * v / allv:.1f}% | {ln} | `{src.replace('|', '/')}` |")
     return out
 
 
@@ -96,6 +140,7 @@ def main():
         lines += launches(a.launches) + [""]
     if a.rep:
         lines += ["## `ncu --set full` capture", ""] + rep(a.rep)
+        lines += ["## Warp-stall samples by source line (top 15)", ""] + stalls(a.rep) + [""]
     open(a.out, "w").write("\n".join(lines) + "\n")
     print("\n".join(lines))
 

@@ -21,6 +21,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--grid", type=int, default=4096)
     ap.add_argument("--rmat", type=int, default=0)
+    ap.add_argument("--ef", type=int, default=16)
+    ap.add_argument("--weights", default="f32", help="rmat weights: f32 (fp32 U[0,1)) or int (1..100, exact path)")
     ap.add_argument("--means", default="2,4,8,16,32")
     ap.add_argument("--caps", default="8", help="nearfar_batches values (continuation batches per warp per round)")
     ap.add_argument("--solves", type=int, default=3)
@@ -36,8 +38,9 @@ def main():
     from paper_2306_07872_b200.devgen import rmat_device_graph
 
     if a.rmat:
-        dg, _, _ = rmat_device_graph(a.rmat, 16, weights="f32", precision="fp32")
-        name = f"rmat{a.rmat}"
+        dg, _, _ = rmat_device_graph(a.rmat, a.ef, weights=a.weights,
+                                     precision="fp32" if a.weights == "f32" else "auto")
+        name = f"rmat{a.rmat}_ef{a.ef}_{a.weights}"
     else:
         dg = D.DeviceGraph.from_csr(G.grid_graph(a.grid, a.grid), precision="auto")
         name = f"grid{a.grid}"
