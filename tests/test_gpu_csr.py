@@ -77,3 +77,16 @@ def test_build_csr_grid_scale(gpu):
     host = P.csr_from_arrays(g.n, u[perm], g.col[perm], g.val[perm])
     assert same_graph(dev, host)
     assert np.array_equal(dev.row_ptr, g.row_ptr)
+
+
+@pytest.mark.parametrize("scale,ef,weights", [(14, 8, "int"), (18, 16, "f32"), (20, 16, "f32")])
+def test_rmat_device_equals_reference_arm_generator(gpu, scale, ef, weights):
+    """dawn_gen_rmat + dawn_build_csr (the bench's GPU arm) == the C generator
+    the reference arm times (oracle rmat_csr): identical CsrGraph arrays."""
+    from oracle import oracle as O
+
+    n, m, rp, col, val = D.rmat_csr_device(scale, ef, weights=weights)
+    on, om, orp, ocol, oval = O.rmat_csr(scale, ef, weights=weights)
+    assert (n, m) == (on, om)
+    assert np.array_equal(rp.cpu().numpy(), orp) and np.array_equal(col.cpu().numpy(), ocol)
+    assert np.array_equal(val.cpu().numpy(), oval)

@@ -193,3 +193,17 @@ def test_rmat_generators_agree_on_host():
         g = G.rmat_graph(scale, ef, weights=w)
         assert (n, m) == (g.n, g.m)
         assert np.array_equal(rp, g.row_ptr) and np.array_equal(col, g.col) and np.array_equal(val, g.val)
+
+
+@pytest.mark.parametrize("scale,ef,weights", [(10, 8, "int"), (12, 8, "int"), (12, 16, "f32"), (14, 8, "int")])
+def test_rmat_generators_identical(scale, ef, weights):
+    """The reference arm's CPU generator (oracle C restatement, O.rmat_csr) and
+    the host generator of the drop-in (generators.rmat_graph) build the SAME
+    CsrGraph bit for bit — so the CPU baseline and the GPU arm time the same
+    graph (the device generator is pinned to both in test_gpu_csr.py)."""
+    from paper_2306_07872_b200 import generators as G
+
+    n, m, rp, col, val = O.rmat_csr(scale, ef, weights=weights)
+    g = G.rmat_graph(scale, ef, weights=weights)
+    assert (n, m) == (g.n, g.m)
+    assert np.array_equal(rp, g.row_ptr) and np.array_equal(col, g.col) and np.array_equal(val, g.val)
