@@ -1114,6 +1114,8 @@ static void fill_stats(const DevState& d, dawn_stats_t* o) {
 static int read_state(dawn_solver_t s, cudaStream_t st) {
   CK(cudaMemcpyAsync(s->st_host, s->st, sizeof(DevState), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  if (s->st_host->abort)
+    return fail(DAWN_ECUDA, "device watchdog: the solve made no progress for 30 s and was aborted");
   return DAWN_OK;
 }
 
@@ -1299,8 +1301,11 @@ extern "C" int dawn_mssp_batch(dawn_solver_t s, const int64_t* sources, int64_t 
   if (stats_out || host_out) {
     CK(cudaStreamSynchronize(st));
     if (stats_out)
-      for (int64_t b = 0; b < nb; ++b)
+      for (int64_t b = 0; b < nb; ++b) {
+        if (s->bst_host[b].abort)
+          return fail(DAWN_ECUDA, "device watchdog: a batch made no progress for 30 s and was aborted");
         fill_batch_stats(s->bst_host[b], (int)std::min<int64_t>(BL, k - b * BL), n, stats_out + b * BL);
+      }
   }
   return DAWN_OK;
 }
@@ -1332,7 +1337,10 @@ extern "C" int dawn_mssp(dawn_solver_t s, const int64_t* sources, int64_t k, int
     if (e != cudaSuccess) rc = fail(DAWN_ECUDA, "mssp: %s", cudaGetErrorString(e));
   }
   if (rc == DAWN_OK && hs)
-    for (int64_t i = 0; i < k; ++i) fill_stats(hs[i], stats_out + i);
+    for (int64_t i = 0; i < k && rc == DAWN_OK; ++i) {
+      if (hs[i].abort) rc = fail(DAWN_ECUDA, "device watchdog: a solve made no progress for 30 s and was aborted");
+      else fill_stats(hs[i], stats_out + i);
+    }
   if (hs) hfree(hs);
   return rc;
 }
@@ -1529,7 +1537,7 @@ extern "C" int dawn_floyd_warshall(int device, int64_t n, const int64_t* row_ptr
   int64_t* d_rp = (int64_t*)(rowb + 2 * n);
   int64_t* d_col = d_rp + (n + 1);
   double* d_val = (double*)(d_col + m);
-  unsigned* flags = (unsigned*)(d_val + m);  // [0] barrier, [1] bad column, [2] negative diagonal
+  unsigned* flags = (unsigned*)(d_val + m);  // [0] barrier, [1] bad column, [2] negative diagonal, [3] abort
   cudaError_t e;
   if ((e = cudaMemcpyAsync(d_rp, row_ptr, 8 * (size_t)(n + 1), cudaMemcpyDefault, st)) != cudaSuccess ||
       (m && (e = cudaMemcpyAsync(d_col, col, 8 * (size_t)m, cudaMemcpyDefault, st)) != cudaSuccess) ||
@@ -1552,11 +1560,12 @@ extern "C" int dawn_floyd_warshall(int device, int64_t n, const int64_t* row_ptr
   if ((e = cudaLaunchCooperativeKernel((void*)fw_steps, dim3(grid), dim3(256), args, 0, st)) != cudaSuccess)
     return release(fail(DAWN_ECUDA, "steps: %s", cudaGetErrorString(e)));
   fw_negdiag<<<(int)std::min<int64_t>(nsm * 4, (n + 255) / 256), 256, 0, st>>>(M, n, flags + 2);
-  unsigned hf[3] = {0, 0, 0};
+  unsigned hf[4] = {0, 0, 0, 0};
   if ((e = cudaMemcpyAsync(out, M, 8 * nn, cudaMemcpyDefault, st)) != cudaSuccess ||
-      (e = cudaMemcpyAsync(hf, flags, 12, cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
+      (e = cudaMemcpyAsync(hf, flags, 16, cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
       (e = cudaStreamSynchronize(st)) != cudaSuccess)
     return release(fail(DAWN_ECUDA, "floyd-warshall: %s", cudaGetErrorString(e)));
+  if (hf[3]) return release(fail(DAWN_ECUDA, "device watchdog: floyd-warshall made no progress for 30 s"));
   if (hf[1]) return release(fail(DAWN_EINVAL, "column index out of range"));
   if (negative_cycle_out) *negative_cycle_out = hf[2] ? 1 : 0;
   return release(DAWN_OK);

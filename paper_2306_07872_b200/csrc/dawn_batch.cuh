@@ -49,6 +49,7 @@ struct BState {
   unsigned bar;                // grid barrier word (never reset)
   unsigned wrote[2];           // lanes that lowered any node in the round with this parity
   unsigned guard;              // lanes whose source guard fired (solver.py:299-303)
+  unsigned abort;              // watchdog: the batch made no progress for 30 s and wound down
   unsigned rounds;             // rounds executed (incl. seeding)
   unsigned lastw[BL];          // per lane: last round that lowered a node (0 = none)
   unsigned long long R[BL], W[BL], FD[BL], MW[BL];
@@ -631,7 +632,7 @@ __global__ void __launch_bounds__(NT, DAWN_BATCH_MIN_BLOCKS) dawn_batch_persiste
       st->le[(r + 1) & 1] = 0ull;
     }
     bphase_build<V, EI, LIVE>(P, r, active, s, accW, accFD, accMW);
-    grid_sync(&st->bar);
+    if (grid_sync(&st->bar, &st->abort)) break;
     // ---- X phase ----
     if (prof) {
       P.prof[4 * r + 1] = globaltimer();
@@ -654,7 +655,7 @@ __global__ void __launch_bounds__(NT, DAWN_BATCH_MIN_BLOCKS) dawn_batch_persiste
     }
     wrote = __reduce_or_sync(0xffffffffu, wrote);
     if (lane == 0 && wrote) atomicOr(&st->wrote[r & 1], wrote);
-    grid_sync(&st->bar);
+    if (grid_sync(&st->bar, &st->abort)) break;
   }
   // ---- per-lane results ----
   if (leader) st->rounds = r - 1;
@@ -714,6 +715,7 @@ __global__ void dawn_batch_init(BParams<V, EI> P) {
     st->le[0] = st->le[1] = 0ull;
     st->wrote[0] = st->wrote[1] = 0u;
     st->guard = 0u;
+    st->abort = 0u;
     st->rounds = 0u;
   }
   if (l < BL) {

@@ -208,9 +208,14 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 
 // Grid-wide barrier for a cooperative (co-resident) launch.  One counter; the
 // arrivals sum to 0x80000000 so the top bit flips exactly once per barrier and
-// the counter never needs a reset.  A watchdog traps instead of hanging the
-// GPU if a CTA never arrives (kills the context -> error on the host).
-__device__ __forceinline__ void grid_sync(unsigned* bar) {
+// the counter never needs a reset.  Watchdog: if the grid makes no progress
+// for 30 s (a CTA never arrives), the waiting CTA sets *abort and leaves the
+// barrier; every CTA sees the flag at its next barrier (returns true) and the
+// kernel winds down cooperatively, so the host gets an error code instead of
+// a sticky device trap that would poison the caller's CUDA context
+// (DAWN_DEBUG_TRAP restores the trap for debugging).
+__device__ __forceinline__ bool grid_sync(unsigned* bar, unsigned* abort) {
+  __shared__ unsigned s_aborted;
   __syncthreads();
   if (threadIdx.x == 0) {
     const unsigned nb = gridDim.x;
@@ -218,17 +223,27 @@ __device__ __forceinline__ void grid_sync(unsigned* bar) {
     __threadfence();
     const unsigned old = atomicAdd(bar, inc);
     unsigned long long t0 = 0;
-    unsigned spins = 0;
+    unsigned spins = 0, ab = 0;
     while (((old ^ ld_acquire(bar)) & 0x80000000u) == 0u) {
       if ((++spins & 4095u) == 0u) {
+        if (ld_acquire(abort)) { ab = 1; break; }
         unsigned long long t = globaltimer();
         if (t0 == 0) t0 = t;
-        else if (t - t0 > 30ull * 1000000000ull) asm volatile("trap;");
+        else if (t - t0 > 30ull * 1000000000ull) {
+#ifdef DAWN_DEBUG_TRAP
+          asm volatile("trap;");
+#endif
+          atomicExch(abort, 1u);
+          ab = 1;
+          break;
+        }
       }
     }
     __threadfence();
+    s_aborted = ab | ld_acquire(abort);
   }
   __syncthreads();
+  return s_aborted != 0u;
 }
 
 // ---------------------------------------------------------------------------
@@ -280,6 +295,7 @@ struct DevState {
   unsigned resume_x;             // stepping: the frontier of `round` is built, resume at its X phase
   unsigned done;
   unsigned flag;                 // negative cycle
+  unsigned abort;                // watchdog: the solve made no progress for 30 s and wound down
   unsigned early;                // stopped by the predecessor-cycle check
   unsigned cyc;                  // scratch for the cycle check
   unsigned long long steps;

@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(256) fw_steps(double* __restrict__ M, int64_t 
         ++i;
       }
     }
-    grid_sync(bar);
+    if (grid_sync(bar, bar + 3)) return;  // [3]: watchdog abort word
   }
 }
 

@@ -854,15 +854,24 @@ __device__ __forceinline__ uint4 wl_item(uint32_t node, uint32_t y, K key) {
 }
 
 // store an item into a reserved slot; waits only if the slot's previous item
-// (one lap back) has not been taken yet
-__device__ __forceinline__ void wl_store(uint4* q, uint32_t pre_node, uint4 item) {
+// (one lap back) has not been taken yet.  Watchdog: after 30 s without the
+// slot freeing (or once another warp gave up) the solve is aborted
+// cooperatively (the host reports DAWN_ECUDA) instead of trapping.
+__device__ __forceinline__ void wl_store(uint4* q, uint32_t pre_node, uint4 item, unsigned* abort) {
   unsigned long long t0 = 0;
   while (pre_node != WL_NONE) {
     __nanosleep(64);
     pre_node = ld_relaxed_u32(&q->x);
+    if (ld_acquire(abort)) return;
     const unsigned long long t = globaltimer();
     if (t0 == 0) t0 = t;
-    else if (t - t0 > 30ull * 1000000000ull) asm volatile("trap;");
+    else if (t - t0 > 30ull * 1000000000ull) {
+#ifdef DAWN_DEBUG_TRAP
+      asm volatile("trap;");
+#endif
+      atomicExch(abort, 1u);
+      return;
+    }
   }
   st_relaxed_v4(q, item);
 }
@@ -894,7 +903,7 @@ __device__ __forceinline__ void wl_push(const KParams<V, EI>& P, const uint32_t 
   for (int j = 0; j < NJ; ++j) {
     if ((msk >> j) & 1u) {
       uint4* q = ring + ((slot0 + t++) & P.wl_mask);
-      wl_store(q, pre[j], wl_item<K>(node[j], deg[j] > CH ? WL_SPLIT : deg[j], key[j]));
+      wl_store(q, pre[j], wl_item<K>(node[j], deg[j] > CH ? WL_SPLIT : deg[j], key[j]), &P.st->abort);
     }
   }
 }
@@ -1140,8 +1149,12 @@ __global__ void __launch_bounds__(NT, 2) dawn_worklist(KParams<V, EI> P) {
             t0 = t;
             seen = ctr;
           } else if (t - t0 > 30ull * 1000000000ull) {
+#ifdef DAWN_DEBUG_TRAP
             asm volatile("trap;");
+#endif
+            atomicExch(&st->abort, 1u);
           }
+          fin = fin || ld_acquire(&st->abort) != 0u;
         }
         if (__shfl_sync(0xffffffffu, fin, 0)) break;
         __nanosleep(ns);
@@ -1201,7 +1214,7 @@ __global__ void __launch_bounds__(NT, 2) dawn_worklist(KParams<V, EI> P) {
         const uint32_t b0 = (uint32_t)__shfl_sync(0xffffffffu, base, 0);
         for (uint32_t c = lane; c < nch; c += 32) {
           uint4* qq = ring + ((b0 + c) & P.wl_mask);
-          wl_store(qq, ld_relaxed_u32(&qq->x), wl_item<K>(lu, WL_CHUNK | c, lk));
+          wl_store(qq, ld_relaxed_u32(&qq->x), wl_item<K>(lu, WL_CHUNK | c, lk), &st->abort);
         }
         __syncwarp();
       } else {
@@ -1259,18 +1272,18 @@ __device__ bool pred_graph_has_cycle(const KParams<V, EI>& P) {
     if (v != src && ldcg(P.dist + v) != VT::INF) j = ~(uint32_t)ldcg(P.pred + v);
     P.jmp0[v] = j;
   }
-  grid_sync(&P.st->bar);
+  if (grid_sync(&P.st->bar, &P.st->abort)) return true;
   uint32_t* a = P.jmp0;
   uint32_t* b = P.jmp1;
   for (int it = 0; it < P.logn; ++it) {
     for (uint32_t v = gtid; v < n; v += gsz) b[v] = ldcg(a + ldcg(a + v));
-    grid_sync(&P.st->bar);
+    if (grid_sync(&P.st->bar, &P.st->abort)) return true;
     uint32_t* t = a; a = b; b = t;
   }
   for (uint32_t v = gtid; v < n; v += gsz) {
     if (v != src && ldcg(P.dist + v) != VT::INF && ldcg(a + v) != src) P.st->cyc = 1u;
   }
-  grid_sync(&P.st->bar);
+  if (grid_sync(&P.st->bar, &P.st->abort)) return true;
   return ldcg(&P.st->cyc) != 0u;
 }
 
@@ -1319,7 +1332,7 @@ __global__ void __launch_bounds__(NT, DAWN_MIN_BLOCKS) dawn_persistent(KParams<V
       }
       if (P.cta_prof != nullptr && r < CTA_PROF_ROUNDS && threadIdx.x == 0)
         P.cta_prof[((size_t)r * 2 + 0) * gridDim.x + blockIdx.x] = globaltimer();
-      grid_sync(&st->bar);
+      if (grid_sync(&st->bar, &st->abort)) break;
       // ---- termination (solver.py:284-285, :313-317, :356-358, :388-395) ----
       if (r >= 2) {
         const unsigned long long wprev = ldcg(&st->wround[p ^ 1]);
@@ -1387,11 +1400,11 @@ __global__ void __launch_bounds__(NT, DAWN_MIN_BLOCKS) dawn_persistent(KParams<V
       __syncthreads();
       if (threadIdx.x == 0) P.cta_prof[((size_t)r * 2 + 1) * gridDim.x + blockIdx.x] = globaltimer();
     }
-    grid_sync(&st->bar);
+    if (grid_sync(&st->bar, &st->abort)) break;
     if (leader) st->resume_x = 0u;  // every CTA has read it (first barrier passed)
     if constexpr (WITH_PRED) {
       phase_expand<V, EI, true, RAW, XI>(P, p, r, dense, s, acc_w, acc_fd, acc_multi, round_w);
-      grid_sync(&st->bar);
+      if (grid_sync(&st->bar, &st->abort)) break;
     }
     if (prof) P.prof[4 * r + 2] = globaltimer();
     dense_prev = dense;
@@ -1450,6 +1463,7 @@ __global__ void dawn_begin_solve(KParams<V, EI> P) {
     st->resume_x = 0u;
     st->done = 0u;
     st->flag = 0u;
+    st->abort = 0u;
     st->early = 0u;
     st->cyc = 0u;
     st->steps = 0ull;

@@ -312,7 +312,7 @@ __global__ void __launch_bounds__(NT, DAWN_MIN_BLOCKS) dawn_nearfar(KParams<V, E
       fmin = CD::INF;
       nearc = 0;
     }
-    grid_sync(&st->bar);
+    if (grid_sync(&st->bar, &st->abort)) break;  // watchdog: wind down, the host reports it
     const unsigned long long nearp = ldcg(&st->nf_near[p]);
     const K fm = (K)ldcg(&st->nf_farmin[p]);
     if (nearp == 0ull) {
