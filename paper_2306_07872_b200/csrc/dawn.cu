@@ -30,6 +30,7 @@
 #include "dawn_csr.cuh"
 #include "dawn_fw.cuh"
 #include "dawn_nearfar.cuh"
+#include "dawn_small.cuh"
 
 using namespace dawn;
 
@@ -191,6 +192,11 @@ struct dawn_solver_s {
   double mean_w = -1;                 // mean edge weight (computed on first near-far solve)
   double nf_cap = 64;                 // tunable "nearfar_batches": continuation batches per warp per round
   int nf_grid = 1;
+  int small_pref = -1;                // tunable "small_graph": -1 auto, 0 off, 1 on (when it fits)
+  bool small = false;                 // unbounded solves without negative weights run dawn_small (one CTA)
+  int small_cl = 0;                   // its cluster size (CTAs)
+  size_t small_smem = 0;
+  bool init_pending = false;          // begin deferred to the small kernel (see Impl::begin)
   double batch_min_sources = 4;       // tunable: dawn_mssp batches when k >= this
   double batch_sparse_util = 4;       // tunable: batched rounds averaging < this active sources per edge go lane-sparse
   int ebits = 32;
@@ -705,6 +711,42 @@ struct Impl {
     int bpw = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpw, dawn_worklist<V, EI>, NT, 0));
     s->wl_grid = std::max(1, bpw) * nsm;
+    // small graphs: one thread-block cluster with the solve state in distributed
+    // shared memory (no negative weights)
+    s->small = false;
+    if (!s->g->has_negative && s->small_pref != 0 && n >= 2 && m < (1ll << 31)) {
+      int optin = 0;
+      CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+      const int dyn_max = optin - 4096;  // static shared memory of the kernel stays below 4 KB
+      for (auto fn : {(const void*)dawn_small<V, EI, false>, (const void*)dawn_small<V, EI, true>}) {
+        CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_max));
+        CK(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+      }
+      s->small_cl = 0;
+      for (int cl = SM_MAXCL; cl >= 1 && !s->small_cl; cl >>= 1) {
+        const size_t need = small_smem_bytes<V, EI>((uint32_t)n, (uint32_t)cl);
+        if (need > (size_t)dyn_max) break;  // a smaller cluster needs even more per CTA
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(cl);
+        cfg.blockDim = dim3(SM_NT);
+        cfg.dynamicSmemBytes = need;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = cl;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        int nc = 0;
+        if (cudaOccupancyMaxActiveClusters(&nc, (const void*)dawn_small<V, EI, false>, &cfg) == cudaSuccess && nc > 0) {
+          s->small_cl = cl;
+          s->small_smem = need;
+        }
+        cudaGetLastError();
+      }
+      // auto: graphs whose rounds are latency-bound on the grid (config 1: 16 K nodes)
+      s->small = s->small_cl > 0 && (s->small_pref > 0 || (n <= (1 << 16) && m <= (1ll << 21)));
+    }
     // near-far schedule (async, no negative weights): on by default where the bitmap frontier is
     s->nf = s->nf_pref < 0 ? s->fb : s->nf_pref > 0;
     int bpn = 0;
@@ -716,7 +758,20 @@ struct Impl {
     return DAWN_OK;
   }
 
+  // the small-graph cluster kernel initialises its own state: its solves skip
+  // the begin kernel unless something else (stepping, a state read) runs first
   static int begin(dawn_solver_t s, cudaStream_t stream) {
+    s->init_pending = false;
+    if (s->small && !(s->run_flags & DAWN_F_PRED) && !s->g->has_negative && !s->prof &&
+        !nearfar_eligible(s, 0xFFFFFFFFu)) {
+      s->init_pending = true;
+      return DAWN_OK;
+    }
+    return init_solve(s, stream);
+  }
+
+  static int init_solve(dawn_solver_t s, cudaStream_t stream) {
+    s->init_pending = false;
     const int64_t n = s->g->n;
     if (s->prof) CK(cudaMemsetAsync(s->prof, 0, 32 * (size_t)s->prof_cap, stream));
     if (s->pred) CK(cudaMemsetAsync(s->pred, 0, sizeof(unsigned long long) * n, stream));
@@ -734,6 +789,29 @@ struct Impl {
   }
 
   static int run(dawn_solver_t s, unsigned max_rounds, cudaStream_t stream) {
+    // async on low-degree graphs: the near-far schedule (far less work than any round schedule)
+    const bool nf = nearfar_eligible(s, max_rounds);
+    if (s->small && !nf && max_rounds == 0xFFFFFFFFu && !(s->run_flags & DAWN_F_PRED) &&
+        !s->g->has_negative) {
+      s->init_pending = false;
+      KParams<V, EI> P = params(s, max_rounds);
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(s->small_cl);
+      cfg.blockDim = dim3(SM_NT);
+      cfg.dynamicSmemBytes = s->small_smem;
+      cfg.stream = stream;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = s->small_cl;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      if (s->run_flags & DAWN_F_ASYNC) CK(cudaLaunchKernelEx(&cfg, dawn_small<V, EI, true>, P));
+      else CK(cudaLaunchKernelEx(&cfg, dawn_small<V, EI, false>, P));
+      return DAWN_OK;
+    }
+    if (s->init_pending) TRY(init_solve(s, stream));
     if (nearfar_eligible(s, max_rounds)) {
       if (s->mean_w < 0) TRY(mean_weight(s, stream));
       KParams<V, EI> P = params(s, max_rounds);
@@ -1047,6 +1125,12 @@ extern "C" int dawn_solver_tune(dawn_solver_t s, const char* key, double value) 
     CK(cudaSetDevice(s->g->device));
     return DISPATCH(s->g, setup(s));
   }
+  if (!strcmp(key, "small_graph")) {
+    if (!(value == -1.0 || value == 0.0 || value == 1.0)) return fail(DAWN_EINVAL, "small_graph must be -1, 0 or 1");
+    s->small_pref = (int)value;
+    CK(cudaSetDevice(s->g->device));
+    return DISPATCH(s->g, setup(s));
+  }
   if (!strcmp(key, "nearfar_delta")) {
     if (!(value >= 0.0)) return fail(DAWN_EINVAL, "nearfar_delta must be >= 0");
     s->nf_delta = value;
@@ -1147,6 +1231,7 @@ extern "C" int dawn_sssp_advance(dawn_solver_t s, int max_rounds, int64_t* round
   if (max_rounds < 1) return fail(DAWN_EINVAL, "max_rounds must be >= 1");
   cudaStream_t st = (cudaStream_t)stream;
   CK(cudaSetDevice(s->g->device));
+  if (s->init_pending) TRY(DISPATCH(s->g, init_solve(s, st)));
   TRY(read_state(s, st));
   if (!s->st_host->done) {
     TRY(DISPATCH(s->g, run(s, (unsigned)max_rounds, st)));
@@ -1169,6 +1254,7 @@ extern "C" int dawn_solver_state(dawn_solver_t s, double* dist_out, uint32_t* st
   if (!s || !s->active) return fail(DAWN_EINVAL, "no active solve");
   cudaStream_t st = (cudaStream_t)stream;
   CK(cudaSetDevice(s->g->device));
+  if (s->init_pending) TRY(DISPATCH(s->g, init_solve(s, st)));
   TRY(DISPATCH(s->g, decode(s, dist_out, nullptr, st)));
   if (stamp_out)
     CK(cudaMemcpyAsync(stamp_out, s->stamp, 4 * (size_t)s->g->n, cudaMemcpyDefault, st));
@@ -1182,6 +1268,7 @@ extern "C" int dawn_solver_result(dawn_solver_t s, double* dist_out, int64_t* pr
   cudaStream_t st = (cudaStream_t)stream;
   CK(cudaSetDevice(s->g->device));
   if (pred_out && !(s->run_flags & DAWN_F_PRED)) return fail(DAWN_EINVAL, "last solve did not record predecessors");
+  if (s->init_pending) TRY(DISPATCH(s->g, init_solve(s, st)));
   TRY(DISPATCH(s->g, decode(s, dist_out, pred_out, st)));
   TRY(read_state(s, st));
   if (stats_out) fill_stats(*s->st_host, stats_out);
@@ -1219,7 +1306,12 @@ extern "C" int dawn_solver_cta_profile(dawn_solver_t s, uint64_t* out, int64_t c
   CK(cudaStreamSynchronize(st));
   const int64_t k = std::min<int64_t>(cap_rounds, (int64_t)CTA_PROF_ROUNDS);
   if (grid_out) *grid_out = s->grid;
+#ifdef DAWN_XTIMING  // debug variant: the per-warp X-phase checkpoints [16][2368][6]
+  if (out) CK(cudaMemcpy(out, s->cta_prof, 8 * (size_t)16 * 2368 * 6, cudaMemcpyDeviceToHost));
+  (void)k;
+#else
   if (out && k > 0) CK(cudaMemcpy(out, s->cta_prof, 8 * 2 * (size_t)s->grid * (size_t)k, cudaMemcpyDeviceToHost));
+#endif
   return DAWN_OK;
 }
 

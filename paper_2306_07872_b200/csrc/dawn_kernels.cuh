@@ -149,16 +149,6 @@ __device__ __forceinline__ void mark_tiles(uint32_t* tile_row, EI off, EI deg, u
   for (EI t = t0; t <= t1; ++t) tile_row[t] = entry;
 }
 
-// first-write bookkeeping of a node lowered in round r (runs exactly once per
-// (node, round)): first_discoveries (solver.py:378-379) and the nodes lowered
-// in >= 2 rounds (updated_ratio numerator, solver.py:258-262).
-__device__ __forceinline__ void count_write(uint8_t* wstate, uint32_t v, unsigned long long& acc_fd,
-                                            unsigned long long& acc_multi) {
-  const uint8_t ws = wstate[v];
-  if (ws == 0) { acc_fd++; wstate[v] = 1; }
-  else if (ws == 1) { acc_multi++; wstate[v] = 2; }
-}
-
 // ---------------------------------------------------------------------------
 // S phase, sparse: snapshot the queue the previous X phase built
 // ---------------------------------------------------------------------------
@@ -576,7 +566,21 @@ __device__ void phase_expand(const KParams<V, EI>& P, int p, uint32_t r, bool de
     if (PRED) pf_node = ldcg(qnode + i0 + lane);
   }
 
+#ifdef DAWN_XTIMING
+  // debug timeline (variant builds only): per round r < 16 and global warp, the
+  // last tile's checkpoints [0] tile start [1] filter done [2] elections back
+  // [3] row bounds / scan done [4] reservation back [5] tile end
+  const uint32_t xt_gw = blockIdx.x * WPB + wid;
+#define XT_MARK(k)                                                                                   \
+  do {                                                                                               \
+    if (P.cta_prof && r < 16 && xt_gw < 2368 && lane == 0)                                           \
+      P.cta_prof[((size_t)r * 2368 + xt_gw) * 6 + (k)] = globaltimer();                              \
+  } while (0)
+#endif
   for (; t < T; t += GW) {
+#ifdef DAWN_XTIMING
+    XT_MARK(0);
+#endif
     const EI e0 = t * (EI)WT;
     const uint32_t len = (E - e0 < (EI)WT) ? (uint32_t)(E - e0) : (uint32_t)WT;
     const uint32_t nrows = il - i0 + 1;
@@ -727,24 +731,44 @@ __device__ void phase_expand(const KParams<V, EI>& P, int p, uint32_t r, bool de
         }
       } else if (__any_sync(0xffffffffu, need != 0u)) {
         // ---- sparse: elect one writer per (node, round), enqueue its row ----
+#ifdef DAWN_XTIMING
+        XT_MARK(1);
+#endif
         unsigned first = 0;
 #pragma unroll
         for (int j = 0; j < XI; ++j)
           if (((need >> j) & 1u) && atomicExch(P.stamp + col[j], r) != r) first |= 1u << j;
+#ifdef DAWN_XTIMING
+        if (__any_sync(0xffffffffu, first != 0u)) XT_MARK(2);
+#endif
         unsigned long long mine = 0;  // (entries << eb) | edges of this lane
-        EI rs[XI];
+        EI rs[XI], re[XI];
+        uint8_t wsv[XI];
+        // every load first (write states, row bounds), all in flight together:
+        // a store before the next element's load would serialise the chain
+        // (the compiler cannot reorder a load above a possibly-aliasing store)
 #pragma unroll
         for (int j = 0; j < XI; ++j) {
-          rs[j] = 0;
+          rs[j] = re[j] = 0;
+          wsv[j] = 0;
+          if ((first >> j) & 1u) {
+            wsv[j] = P.wstate[col[j]];
+            rs[j] = __ldg(P.row_ptr + col[j]);
+            re[j] = __ldg(P.row_ptr + col[j] + 1);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < XI; ++j) {
           if ((first >> j) & 1u) {
             round_w++;
             acc_w++;
-            count_write(P.wstate, col[j], acc_fd, acc_multi);
-            const EI a = __ldg(P.row_ptr + col[j]), b = __ldg(P.row_ptr + col[j] + 1);
-            rs[j] = a;
-            if (b > a) {  // rows without edges never need a rescan
-              mine += (1ull << eb) + (unsigned long long)(b - a);
-              wv[j] = (WB)(b - a);  // reuse: degree
+            // first-write bookkeeping (runs once per (node, round)): first_discoveries
+            // (solver.py:378-379) and nodes lowered in >= 2 rounds (solver.py:258-262)
+            if (wsv[j] == 0) { acc_fd++; P.wstate[col[j]] = 1; }
+            else if (wsv[j] == 1) { acc_multi++; P.wstate[col[j]] = 2; }
+            if (re[j] > rs[j]) {  // rows without edges never need a rescan
+              mine += (1ull << eb) + (unsigned long long)(re[j] - rs[j]);
+              wv[j] = (WB)(re[j] - rs[j]);  // reuse: degree
             } else {
               first &= ~(1u << j);
             }
@@ -757,10 +781,16 @@ __device__ void phase_expand(const KParams<V, EI>& P, int p, uint32_t r, bool de
           if (lane >= (uint32_t)d) incl += y;
         }
         const unsigned long long tot = __shfl_sync(0xffffffffu, incl, 31);
+#ifdef DAWN_XTIMING
+        XT_MARK(3);
+#endif
         if (tot) {
           unsigned long long base = 0;
           if (lane == 0) base = atomicAdd(&P.st->res[np], tot);
           base = __shfl_sync(0xffffffffu, base, 0);
+#ifdef DAWN_XTIMING
+          XT_MARK(4);
+#endif
           const unsigned long long at = base + incl - mine;
           uint32_t pos = (uint32_t)pk_count(at, eb);
           EI off = (EI)pk_edges(at, eb);
@@ -792,6 +822,9 @@ __device__ void phase_expand(const KParams<V, EI>& P, int p, uint32_t r, bool de
       }
     }
     __syncwarp();  // the warp is done with its rows / marks
+#ifdef DAWN_XTIMING
+    XT_MARK(5);
+#endif
   }
 }
 
@@ -1330,8 +1363,10 @@ __global__ void __launch_bounds__(NT, DAWN_MIN_BLOCKS) dawn_persistent(KParams<V
       } else {
         phase_snapshot<V, EI, XI>(P, p);
       }
+#ifndef DAWN_XTIMING
       if (P.cta_prof != nullptr && r < CTA_PROF_ROUNDS && threadIdx.x == 0)
         P.cta_prof[((size_t)r * 2 + 0) * gridDim.x + blockIdx.x] = globaltimer();
+#endif
       if (grid_sync(&st->bar, &st->abort)) break;
       // ---- termination (solver.py:284-285, :313-317, :356-358, :388-395) ----
       if (r >= 2) {
@@ -1396,10 +1431,12 @@ __global__ void __launch_bounds__(NT, DAWN_MIN_BLOCKS) dawn_persistent(KParams<V
     phase_expand<V, EI, false, RAW, XI, FB>(P, p, r, dense, s, acc_w, acc_fd, acc_multi, round_w);
     round_w = __reduce_add_sync(0xffffffffu, round_w);
     if ((threadIdx.x & 31) == 0 && round_w) atomicAdd(&st->wround[p], (unsigned long long)round_w);
+#ifndef DAWN_XTIMING
     if (P.cta_prof != nullptr && r < CTA_PROF_ROUNDS) {
       __syncthreads();
       if (threadIdx.x == 0) P.cta_prof[((size_t)r * 2 + 1) * gridDim.x + blockIdx.x] = globaltimer();
     }
+#endif
     if (grid_sync(&st->bar, &st->abort)) break;
     if (leader) st->resume_x = 0u;  // every CTA has read it (first barrier passed)
     if constexpr (WITH_PRED) {

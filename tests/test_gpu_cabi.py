@@ -66,6 +66,7 @@ def test_repeated_create_destroy_and_worklist_stats(gpu):
         h, keep = make(g, N.F32, pinned=it % 2 == 1)
         s = C.c_void_p()
         N.check(L.dawn_solver_create(h, 0, C.byref(s)))
+        N.check(L.dawn_solver_tune(s, b"small_graph", 0.0))  # the worklist lives in the persistent kernels
         d = torch.empty(g.n, dtype=torch.float64, device="cuda")
         N.check(L.dawn_sssp(s, 0, N.GOVM, N.F_ASYNC, d.data_ptr(), None, None, None))
         wl = (C.c_uint64 * 6)()

@@ -25,9 +25,9 @@ def same(a, b) -> bool:
 @pytest.fixture
 def nearfar():
     """Force the near-far path (auto enables it only on low-degree graphs with n >= 4096)."""
-    P.set_tuning(nearfar=1)
+    P.set_tuning(nearfar=1, small_graph=0)
     yield
-    P.set_tuning(nearfar=-1, nearfar_delta=0, nearfar_delta_mean=8)
+    P.set_tuning(nearfar=-1, nearfar_delta=0, nearfar_delta_mean=8, small_graph=-1)
 
 
 def _vtype(w, precision):

@@ -223,16 +223,19 @@ def test_determinism_and_stream_reuse(gpu):
 # ---------------------------------------------------------------------------
 # randomized parity against the oracle, all value types
 # ---------------------------------------------------------------------------
-@pytest.fixture(params=[(0.5, -1, -1), (0.0, 1, 0), (1e9, 1, 0), (0.0, 0, 0), (1e9, 0, 1), (0.5, 0, 1)],
-                ids=["auto", "all-dense-wide", "all-sparse-wide", "all-dense-narrow", "all-bitmap", "mixed-bitmap"])
+@pytest.fixture(params=[(0.5, -1, -1, -1), (0.0, 1, 0, 0), (1e9, 1, 0, 0), (0.0, 0, 0, 0), (1e9, 0, 1, 0),
+                        (0.5, 0, 1, 0), (0.5, -1, -1, 1)],
+                ids=["auto", "all-dense-wide", "all-sparse-wide", "all-dense-narrow", "all-bitmap", "mixed-bitmap",
+                     "small-cta"])
 def frontier_mode(request):
-    """Run under the default frontier / tile-width policy and the extremes:
-    stamps (dense) vs enqueue (sparse) vs bitmap light-round frontiers,
-    14- vs 8-edge-per-lane tiles."""
-    dense, wide, fb = request.param
-    P.set_tuning(dense_edges_per_node=dense, wide_tiles=wide, bitmap_frontier=fb)
+    """Run under the default policy and the extremes of the persistent kernel
+    (the one-CTA small-graph kernel off): stamps (dense) vs enqueue (sparse) vs
+    bitmap light-round frontiers, 14- vs 8-edge-per-lane tiles; and the
+    small-graph kernel forced on wherever it fits."""
+    dense, wide, fb, small = request.param
+    P.set_tuning(dense_edges_per_node=dense, wide_tiles=wide, bitmap_frontier=fb, small_graph=small)
     yield request.param
-    P.set_tuning(dense_edges_per_node=0.5, wide_tiles=-1, bitmap_frontier=-1)
+    P.set_tuning(dense_edges_per_node=0.5, wide_tiles=-1, bitmap_frontier=-1, small_graph=-1)
 
 
 @pytest.mark.parametrize("seed", range(24))

@@ -21,9 +21,9 @@ DEFAULT = float(1 << 20)
 
 @pytest.fixture(params=[0.0, DEFAULT, 1e18], ids=["off", "default", "always"])
 def wl(request):
-    P.set_tuning(worklist_edges=request.param)
+    P.set_tuning(worklist_edges=request.param, small_graph=0)  # the worklist lives in the persistent kernels
     yield request.param
-    P.set_tuning(worklist_edges=DEFAULT)
+    P.set_tuning(worklist_edges=DEFAULT, small_graph=-1)
 
 
 def same(a, b) -> bool:
