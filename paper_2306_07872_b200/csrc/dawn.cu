@@ -195,6 +195,7 @@ struct dawn_solver_s {
   int small_pref = -1;                // tunable "small_graph": -1 auto, 0 off, 1 on (when it fits)
   bool small = false;                 // unbounded solves without negative weights run dawn_small (one CTA)
   int small_cl = 0;                   // its cluster size (CTAs)
+  int small_cl_max = SM_MAXCL;        // tunable "small_cluster": largest cluster to try (power of two)
   size_t small_smem = 0;
   bool init_pending = false;          // begin deferred to the small kernel (see Impl::begin)
   double batch_min_sources = 4;       // tunable: dawn_mssp batches when k >= this
@@ -723,7 +724,7 @@ struct Impl {
         CK(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
       }
       s->small_cl = 0;
-      for (int cl = SM_MAXCL; cl >= 1 && !s->small_cl; cl >>= 1) {
+      for (int cl = s->small_cl_max; cl >= 1 && !s->small_cl; cl >>= 1) {
         const size_t need = small_smem_bytes<V, EI>((uint32_t)n, (uint32_t)cl);
         if (need > (size_t)dyn_max) break;  // a smaller cluster needs even more per CTA
         cudaLaunchConfig_t cfg = {};
@@ -745,7 +746,7 @@ struct Impl {
         cudaGetLastError();
       }
       // auto: graphs whose rounds are latency-bound on the grid (config 1: 16 K nodes)
-      s->small = s->small_cl > 0 && (s->small_pref > 0 || (n <= (1 << 16) && m <= (1ll << 21)));
+      s->small = s->small_cl > 0 && (s->small_pref > 0 || (n <= (1 << 16) && m <= (1ll << 18)));
     }
     // near-far schedule (async, no negative weights): on by default where the bitmap frontier is
     s->nf = s->nf_pref < 0 ? s->fb : s->nf_pref > 0;
@@ -1128,6 +1129,13 @@ extern "C" int dawn_solver_tune(dawn_solver_t s, const char* key, double value) 
   if (!strcmp(key, "small_graph")) {
     if (!(value == -1.0 || value == 0.0 || value == 1.0)) return fail(DAWN_EINVAL, "small_graph must be -1, 0 or 1");
     s->small_pref = (int)value;
+    CK(cudaSetDevice(s->g->device));
+    return DISPATCH(s->g, setup(s));
+  }
+  if (!strcmp(key, "small_cluster")) {
+    if (!(value == 1.0 || value == 2.0 || value == 4.0 || value == 8.0 || value == 16.0))
+      return fail(DAWN_EINVAL, "small_cluster must be 1, 2, 4, 8 or 16");
+    s->small_cl_max = (int)value;
     CK(cudaSetDevice(s->g->device));
     return DISPATCH(s->g, setup(s));
   }

@@ -36,7 +36,10 @@
 namespace dawn {
 
 constexpr int SM_NT = 1024;      // threads per CTA
-constexpr int SM_NS = 4;         // edges in flight per thread in the relax
+#ifndef DAWN_SM_NS
+#define DAWN_SM_NS 4
+#endif
+constexpr int SM_NS = DAWN_SM_NS;         // edges in flight per thread in the relax
 constexpr int SM_RUN = 4;        // S phase: owned nodes per thread whose row bounds stay in registers
 constexpr int SM_MAXCL = 16;      // cluster size (non-portable above 8)
 
