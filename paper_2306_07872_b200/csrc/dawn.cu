@@ -198,6 +198,7 @@ struct dawn_solver_s {
   int small_cl_max = SM_MAXCL;        // tunable "small_cluster": largest cluster to try (power of two)
   size_t small_smem = 0;
   bool init_pending = false;          // begin deferred to the small kernel (see Impl::begin)
+  bool spec = true;                   // tunable "speculate_negcheck": negative-weight solves try the plain kernel first
   double batch_min_sources = 4;       // tunable: dawn_mssp batches when k >= this
   double batch_sparse_util = 4;       // tunable: batched rounds averaging < this active sources per edge go lane-sparse
   int ebits = 32;
@@ -634,6 +635,7 @@ struct Impl {
     P.nf_delta = s->nf_delta > 0 ? s->nf_delta : s->nf_delta_mean * std::max(s->mean_w, 0.0);
     if (!(P.nf_delta > 0)) P.nf_delta = std::is_floating_point<V>::value ? 1e-3 : 1.0;
     P.nf_cap = (uint32_t)std::min(s->nf_cap, 4.0e9);
+    P.skip_if_done = 0;
     return P;
   }
 
@@ -813,6 +815,36 @@ struct Impl {
       return DAWN_OK;
     }
     if (s->init_pending) TRY(init_solve(s, stream));
+    // Integer graphs with negative weights run the predecessor-tracking kernel
+    // (a second relax pass per round) only for the cycle check every
+    // negcheck_period rounds.  Speculate first: the plain kernel runs the same
+    // rounds up to the first check; a solve that converges by then (no
+    // negative cycle: the common case, config 5a) is finished and the two
+    // launches behind it return at once; otherwise the state is reset on the
+    // device and the tracking kernel solves from scratch.  No host sync.
+    {
+      KParams<V, EI> P = params(s, max_rounds);
+      if (P.negcheck_period > 0 && !(s->run_flags & DAWN_F_PRED) && max_rounds == 0xFFFFFFFFu && s->spec) {
+        KParams<V, EI> Q = P;
+        Q.pred_on = 0;
+        Q.negcheck_period = 0;
+        Q.live = 0;
+        Q.wl_ring = nullptr;
+        Q.max_rounds = (unsigned)P.negcheck_period;
+        void* qa[] = {&Q};
+        CK(cudaLaunchCooperativeKernel(kernel_for(s, false), dim3(s->grid), dim3(NT), qa, s->smem, stream));
+        KParams<V, EI> B = P;
+        B.skip_if_done = 1;
+        const int64_t n = s->g->n;
+        const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(148 * 8, (n + 255) / 256));
+        dawn_begin_solve<V, EI, false><<<blocks, 256, 0, stream>>>(B);  // negative weights: sign-flip keys
+        CK(cudaGetLastError());
+        P.skip_if_done = 1;
+        void* pa[] = {&P};
+        CK(cudaLaunchCooperativeKernel(kernel_for(s, true), dim3(s->grid_pred), dim3(NT), pa, s->smem, stream));
+        return DAWN_OK;
+      }
+    }
     if (nearfar_eligible(s, max_rounds)) {
       if (s->mean_w < 0) TRY(mean_weight(s, stream));
       KParams<V, EI> P = params(s, max_rounds);
@@ -1131,6 +1163,11 @@ extern "C" int dawn_solver_tune(dawn_solver_t s, const char* key, double value) 
     s->small_pref = (int)value;
     CK(cudaSetDevice(s->g->device));
     return DISPATCH(s->g, setup(s));
+  }
+  if (!strcmp(key, "speculate_negcheck")) {
+    if (!(value == 0.0 || value == 1.0)) return fail(DAWN_EINVAL, "speculate_negcheck must be 0 or 1");
+    s->spec = value != 0.0;
+    return DAWN_OK;
   }
   if (!strcmp(key, "small_cluster")) {
     if (!(value == 1.0 || value == 2.0 || value == 4.0 || value == 8.0 || value == 16.0))

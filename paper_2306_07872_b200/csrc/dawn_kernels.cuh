@@ -67,6 +67,8 @@ struct KParams {
   unsigned prof_cap;                   // rounds the timeline can hold
   unsigned long long* cta_prof;        // debug: per-CTA S/X work end times [round][2][grid], or nullptr
   int live;                            // async schedule: frontier rows relaxed with their live value (no snapshot)
+  int skip_if_done;                    // speculative negative-weight solves: return at once if a previous
+                                       // launch already finished the solve (see Impl::run)
   // worklist tail (async schedule, non-negative weights, unbounded run): once a
   // round relaxes < wl_edges edges the rest of the solve runs barrier-free
   unsigned long long* wl_ring;         // ring of 16-byte row items (uint4); nullptr = off
@@ -1333,6 +1335,7 @@ __global__ void __launch_bounds__(NT, DAWN_MIN_BLOCKS) dawn_persistent(KParams<V
   Smem<V, EI, XI>& s = *reinterpret_cast<Smem<V, EI, XI>*>(smem_raw);
   DevState* st = P.st;
   const bool leader = (blockIdx.x == 0 && threadIdx.x == 0);
+  if (P.skip_if_done && ldcg(&st->done)) return;  // uniform: written by an earlier launch
 
   uint32_t r = ldcg(&st->round);
   bool dense_prev = ldcg(&st->dense_prev) != 0u;  // how round r-1 recorded its writes
@@ -1472,6 +1475,7 @@ template <class V, class EI, bool RAW>
 __global__ void dawn_begin_solve(KParams<V, EI> P) {
   using CD = Codec<V, RAW>;
   using K = typename CD::K;
+  if (P.skip_if_done && ldcg(&P.st->done)) return;  // the speculative run converged: keep its result
   const uint32_t n = P.n;
   const size_t T = (size_t)gridDim.x * blockDim.x;
   const size_t t0 = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
