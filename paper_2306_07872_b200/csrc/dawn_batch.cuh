@@ -298,16 +298,17 @@ __device__ void bphase_build(const BParams<V, EI>& P, uint32_t r, uint32_t activ
 #pragma unroll 1
     for (int q = 0; q < (LIVE ? 2 : 1); ++q) {
       const unsigned qs = q ? sel_s : sel;
-      if (!qs) continue;
+      if (!__any_sync(0xffffffffu, qs != 0u)) continue;  // warp-uniform: the tile marks are warp-collective
       const unsigned long long at = q ? s.basepk_s + incl_s - mine_s : s.basepk + incl - mine;
       uint32_t pos = (uint32_t)pk_count(at, eb);
       EI off = (EI)pk_edges(at, eb);
       constexpr int NV = BL * (int)sizeof(K) / 16;
 #pragma unroll
       for (int j = 0; j < ITEMS; ++j) {
-        if ((qs >> j) & 1u) {
+        const bool has = (qs >> j) & 1u;
+        const EI dg = has ? rp[j + 1] - rp[j] : (EI)0;
+        if (has) {
           const uint32_t v = u0 + j;
-          const EI dg = rp[j + 1] - rp[j];
           const uint4* srcl = reinterpret_cast<const uint4*>(P.bd + (size_t)v * BL);
           uint4* dstl = reinterpret_cast<uint4*>(P.qkey + (size_t)pos * BL);
           uint4 x[8];
@@ -319,11 +320,6 @@ __device__ void bphase_build(const BParams<V, EI>& P, uint32_t r, uint32_t activ
           P.qmask[q][pos] = F[j];
           P.qoff[q][pos] = off;
           P.qbase[q][pos] = rp[j] - off;
-          {
-            const EI t0 = (off + (EI)(BWT - 1)) / (EI)BWT;
-            const EI t1 = (off + dg - 1) / (EI)BWT;
-            for (EI tt = t0; tt <= t1; ++tt) P.tile_row[q][tt] = pos;
-          }
           if (!LIVE) {  // the async schedule reads the live line instead
 #pragma unroll
             for (int qq = 0; qq < 8; ++qq) dstl[qq] = x[qq];
@@ -335,6 +331,9 @@ __device__ void bphase_build(const BParams<V, EI>& P, uint32_t r, uint32_t activ
               for (int qq = 0; qq < 8; ++qq) dstl[h + qq] = x[qq];
             }
           }
+        }
+        mark_tiles_warp<BWT, EI>(P.tile_row[q], has, off, dg, pos);
+        if (has) {
           pos++;
           off += dg;
         }

@@ -151,6 +151,36 @@ __device__ __forceinline__ void mark_tiles(uint32_t* tile_row, EI off, EI deg, u
   for (EI t = t0; t <= t1; ++t) tile_row[t] = entry;
 }
 
+// Warp-collective mark_tiles (every lane calls it; `has` = this lane has a row):
+// short rows are marked by their lane, rows spanning >= 32 tiles by the whole
+// warp.  Used by the batched kernel, whose 32-edge tiles make a hub row
+// (10^5 edges = thousands of tiles) hold one thread — and its CTA, and the
+// grid barrier behind it — for ~10 us.  (The single-source S phases keep the
+// per-lane loop: their tiles are 8-14x wider and the warp vote cost more
+// than it saved on config 2.)
+template <int WT, class EI>
+__device__ __forceinline__ void mark_tiles_warp(uint32_t* tile_row, bool has, EI off, EI deg, uint32_t entry) {
+  EI t0 = 0, t1 = 0;
+  bool lng = false;
+  if (has && deg > 0) {
+    t0 = (off + (EI)(WT - 1)) / (EI)WT;
+    t1 = (off + deg - 1) / (EI)WT;
+    if (t1 >= t0 + (EI)32) lng = true;
+    else
+      for (EI t = t0; t <= t1; ++t) tile_row[t] = entry;
+  }
+  unsigned lm = __ballot_sync(0xffffffffu, lng);
+  const uint32_t lane = threadIdx.x & 31;
+  while (lm) {
+    const int L = __ffs(lm) - 1;
+    lm &= lm - 1u;
+    const EI a = (EI)__shfl_sync(0xffffffffu, (unsigned long long)t0, L);
+    const EI b = (EI)__shfl_sync(0xffffffffu, (unsigned long long)t1, L);
+    const uint32_t e = __shfl_sync(0xffffffffu, entry, L);
+    for (EI t = a + (EI)lane; t <= b; t += (EI)32) tile_row[t] = e;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // S phase, sparse: snapshot the queue the previous X phase built
 // ---------------------------------------------------------------------------
