@@ -173,3 +173,23 @@ def test_batch_async_rmat_and_api(gpu):
     assert agg is not None
     with pytest.raises(ValueError):
         P.mssp(gi, [0], schedule="chaotic")
+
+
+def test_results_survive_later_calls_of_the_same_size(gpu):
+    """Pooled page-locked result blocks: rows and slices of an
+    earlier result must not be overwritten by a later call of the same size."""
+    g = G.rmat_graph(10, 8, weights="int")
+    a = P.mssp(g, [0, 1])
+    a_rows = [dv.dist.copy() for dv, _ in a]
+    view = a[0][0].dist[: g.n // 2]
+    view_copy = view.copy()
+    for srcs in ([2, 3], [4, 5], [6, 7], [8, 9], [10, 11]):
+        P.mssp(g, srcs)
+    d1 = P.govm_sssp(g, 5)[0].dist
+    keep = d1[:10]
+    P.mssp(g, [12])
+    P.govm_sssp(g, 7)
+    for (dv, _), ref in zip(a, a_rows):
+        assert np.array_equal(dv.dist, ref)
+    assert np.array_equal(view, view_copy)
+    assert np.array_equal(keep, P.govm_sssp(g, 5)[0].dist[:10])
