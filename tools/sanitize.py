@@ -35,8 +35,9 @@ def main():
     neg, _ = G.johnson_reweight(G.rmat_graph(10, 8), pseed=3)
     cyc = G.inject_cycles(neg, 1, source=0, seed=7)
     checked = 0
-    for mode in ((0.5, -1, -1), (1e9, 0, 1), (0.0, 1, 0), (1e9, 1, 0)):
-        P.set_tuning(dense_edges_per_node=mode[0], wide_tiles=mode[1], bitmap_frontier=mode[2])
+    # round-1 kernel modes with the small-graph cluster kernel off, then the cluster kernel forced on
+    for mode in ((0.5, -1, -1, 0), (1e9, 0, 1, 0), (0.0, 1, 0, 0), (1e9, 1, 0, 0), (0.5, -1, -1, 1)):
+        P.set_tuning(dense_edges_per_node=mode[0], wide_tiles=mode[1], bitmap_frontier=mode[2], small_graph=mode[3])
         for g in graphs:
             for prec in ("auto", "fp32", "fp64"):
                 for algo in ("govm", "gsvm"):
@@ -52,12 +53,26 @@ def main():
             MS.mssp_tile(g, list(range(40)), "govm", schedule="async")
             MS.mssp_tile(g, list(range(7)), "gsvm")
             checked += 4
-    P.set_tuning(dense_edges_per_node=0.5, wide_tiles=-1, bitmap_frontier=-1)
-    for g in (neg, cyc):
-        P.govm_sssp(g, 0)
-        P.govm_sssp(g, 0, record_pred=True)
-        P.gsvm_sssp(g, 0)
-        checked += 3
+    P.set_tuning(dense_edges_per_node=0.5, wide_tiles=-1, bitmap_frontier=-1, small_graph=-1)
+    for spec in (1, 0):  # negative weights: speculative plain kernel first / tracking kernel only
+        P.set_tuning(speculate_negcheck=spec)
+        for g in (neg, cyc):
+            P.govm_sssp(g, 0)
+            P.govm_sssp(g, 0, record_pred=True)
+            P.gsvm_sssp(g, 0)
+            checked += 3
+    P.set_tuning(speculate_negcheck=1)
+    # the near-far kernel (async, low degree): grid default, forced on an RMAT, tiny / huge buckets
+    P.set_tuning(small_graph=0)
+    for delta in (0.0, 1.0, 1e9):
+        P.set_tuning(nearfar_delta=delta)
+        P.govm_sssp(graphs[2], 0, schedule="async")
+        checked += 1
+    P.set_tuning(nearfar=1, nearfar_delta=0)
+    P.govm_sssp(graphs[3], 0, precision="fp32", schedule="async")
+    P.govm_sssp(graphs[0], 0, schedule="async")
+    P.set_tuning(nearfar=-1, small_graph=-1)
+    checked += 2
     u = rng.integers(0, 1000, 20000)
     v = rng.integers(0, 1000, 20000)
     D.build_csr_device(1000, u, v, rng.uniform(0, 1, 20000))
@@ -65,7 +80,7 @@ def main():
     P.floyd_warshall_apsp(neg if neg.n <= 2000 else graphs[1])
     big = G.rmat_graph(16, 80, weights="f32")  # m >= 2^22: chunked DMA upload path
     P.govm_sssp(big, 0, precision="fp32", schedule="async")
-    print(f"sanitize: {checked} solves + batches + csr build + floyd-warshall + staged upload ran")
+    print(f"sanitize: {checked} solves (persistent, worklist, near-far, small-graph cluster, speculative negative-weight) + batches + csr build + floyd-warshall + staged upload ran")
 
 
 if __name__ == "__main__":
