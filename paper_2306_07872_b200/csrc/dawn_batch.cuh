@@ -145,37 +145,37 @@ __device__ void bphase_build(const BParams<V, EI>& P, uint32_t r, uint32_t activ
   for (uint32_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
     const uint32_t u0 = c * TILE + threadIdx.x * ITEMS;
     const bool full = u0 + ITEMS <= n;
-    uint32_t M[ITEMS];
-    if (full) ldcg8<uint32_t>(P.nmask + u0, M);
-    else {
+    // every load of the chunk up front (lane masks, write states, row bounds):
+    // conditional loads behind each other — and behind the bookkeeping stores,
+    // which the compiler cannot reorder them past — made a serial chain
+    uint32_t M[ITEMS], W1[ITEMS], W2[ITEMS];
+    EI rp[ITEMS + 1];
+    if (full) {
+      ldcg8<uint32_t>(P.nmask + u0, M);
+      ldcg8<uint32_t>(P.w1 + u0, W1);
+      ldcg8<uint32_t>(P.w2 + u0, W2);
+      ldg8<EI>(P.row_ptr + u0, *reinterpret_cast<EI(*)[ITEMS]>(rp));
+      rp[ITEMS] = __ldg(P.row_ptr + u0 + ITEMS);
+    } else {
 #pragma unroll
-      for (int j = 0; j < ITEMS; ++j) M[j] = (u0 + j < n) ? ldcg(P.nmask + u0 + j) : 0u;
+      for (int j = 0; j < ITEMS; ++j) {
+        const bool in = u0 + j < n;
+        M[j] = in ? ldcg(P.nmask + u0 + j) : 0u;
+        W1[j] = in ? ldcg(P.w1 + u0 + j) : 0u;
+        W2[j] = in ? ldcg(P.w2 + u0 + j) : 0u;
+        rp[j] = (u0 + j <= n) ? __ldg(P.row_ptr + u0 + j) : (EI)0;
+      }
+      rp[ITEMS] = (u0 + ITEMS <= n) ? __ldg(P.row_ptr + u0 + ITEMS) : (EI)0;
     }
     uint32_t anyM = 0;
 #pragma unroll
     for (int j = 0; j < ITEMS; ++j) anyM |= M[j];
-    uint32_t W1[ITEMS];
-#pragma unroll
-    for (int j = 0; j < ITEMS; ++j) W1[j] = 0;
-    if (anyM || gsvm) {
-      if (full) ldcg8<uint32_t>(P.w1 + u0, W1);
-      else {
-#pragma unroll
-        for (int j = 0; j < ITEMS; ++j) W1[j] = (u0 + j < n) ? ldcg(P.w1 + u0 + j) : 0u;
-      }
-    }
     if (r >= 2) {
       // ---- write bookkeeping of round r-1 (the seeding round's frontier is not a write) ----
       uint32_t FDm[ITEMS], MWm[ITEMS];
 #pragma unroll
       for (int j = 0; j < ITEMS; ++j) { FDm[j] = 0; MWm[j] = 0; }
       if (anyM) {
-        uint32_t W2[ITEMS];
-        if (full) ldcg8<uint32_t>(P.w2 + u0, W2);
-        else {
-#pragma unroll
-          for (int j = 0; j < ITEMS; ++j) W2[j] = (u0 + j < n) ? ldcg(P.w2 + u0 + j) : 0u;
-        }
 #pragma unroll
         for (int j = 0; j < ITEMS; ++j) {
           FDm[j] = M[j] & ~W1[j];
@@ -240,19 +240,10 @@ __device__ void bphase_build(const BParams<V, EI>& P, uint32_t r, uint32_t activ
     uint32_t anyF = 0;
 #pragma unroll
     for (int j = 0; j < ITEMS; ++j) anyF |= F[j];
-    EI rp[ITEMS + 1];
     unsigned sel = 0, sel_s = 0;  // rows of list 0 / list 1 (few active sources, async)
     uint32_t mycnt = 0, mycnt_s = 0;
     EI mydeg = 0, mydeg_s = 0;
     if (anyF) {
-      if (full) {
-        ldg8<EI>(P.row_ptr + u0, *reinterpret_cast<EI(*)[ITEMS]>(rp));
-        rp[ITEMS] = __ldg(P.row_ptr + u0 + ITEMS);
-      } else {
-#pragma unroll
-        for (int j = 0; j < ITEMS; ++j) rp[j] = (u0 + j <= n) ? __ldg(P.row_ptr + u0 + j) : (EI)0;
-        rp[ITEMS] = (u0 + ITEMS <= n) ? __ldg(P.row_ptr + u0 + ITEMS) : (EI)0;
-      }
 #pragma unroll
       for (int j = 0; j < ITEMS; ++j) {
         if (F[j] && u0 + j < n && rp[j + 1] > rp[j]) {
