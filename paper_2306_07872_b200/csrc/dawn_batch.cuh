@@ -382,11 +382,20 @@ struct BRows {        // row metadata of a tile in flight
   uint32_t rnode;
 };
 
+// the row range [i0, il] of tile t (first stage of a row load)
+template <class V, class EI>
+__device__ __forceinline__ void brows_bounds(const BParams<V, EI>& P, int q, EI t, EI T, uint32_t cnt,
+                                             uint32_t& i0, uint32_t& il) {
+  i0 = __ldca(P.tile_row[q] + t);
+  il = (t + 1 < T) ? __ldca(P.tile_row[q] + t + 1) : cnt - 1;
+}
+
+// the rows' metadata once the range is known (second stage)
 template <class V, class EI, bool LIVE>
-__device__ __forceinline__ void brows_load(const BParams<V, EI>& P, int q, EI t, EI T, uint32_t cnt, uint32_t lane,
-                                           BRows<V, EI>& R) {
-  R.i0 = __ldca(P.tile_row[q] + t);
-  R.il = (t + 1 < T) ? __ldca(P.tile_row[q] + t + 1) : cnt - 1;
+__device__ __forceinline__ void brows_finish(const BParams<V, EI>& P, int q, uint32_t i0, uint32_t il, uint32_t lane,
+                                             BRows<V, EI>& R) {
+  R.i0 = i0;
+  R.il = il;
   R.off = 0;
   R.base = 0;
   R.rmask = 0;
@@ -397,6 +406,14 @@ __device__ __forceinline__ void brows_load(const BParams<V, EI>& P, int q, EI t,
     R.rmask = __ldca(P.qmask[q] + R.i0 + lane);
     if (LIVE) R.rnode = __ldca(P.qnode[q] + R.i0 + lane);
   }
+}
+
+template <class V, class EI, bool LIVE>
+__device__ __forceinline__ void brows_load(const BParams<V, EI>& P, int q, EI t, EI T, uint32_t cnt, uint32_t lane,
+                                           BRows<V, EI>& R) {
+  uint32_t i0, il;
+  brows_bounds<V, EI>(P, q, t, T, cnt, i0, il);
+  brows_finish<V, EI, LIVE>(P, q, i0, il, lane, R);
 }
 
 // row of every edge (row-start bits + popc), then the edge loads
@@ -453,8 +470,9 @@ __device__ void bphase_expand(const BParams<V, EI>& P, int q, uint32_t r, const 
   const EI GW = (EI)gridDim.x * WPB;
   EI t = (EI)blockIdx.x * WPB + wid;
   if (t >= T) return;  // warp-uniform
-  // software pipeline (depth 2): edges of tile t and t+GW in flight, rows of
-  // t+2GW in flight, while tile t's distance lines are gathered and relaxed
+  // software pipeline (depth 3): edges of tile t and t+GW in flight, rows of
+  // t+2GW in flight and the row range of t+3GW, while tile t's distance lines
+  // are gathered and relaxed
   BTile<WB> A, Bt;
   BRows<V, EI> Rn;
   {
@@ -470,6 +488,9 @@ __device__ void bphase_expand(const BParams<V, EI>& P, int q, uint32_t r, const 
   }
   bool have_rn = t + 2 * GW < T;
   if (have_rn) brows_load<V, EI, LIVE>(P, q, t + 2 * GW, T, cnt, lane, Rn);
+  // and the row range of t+3GW (its metadata loads wait on it: one stage ahead)
+  uint32_t nb_i0 = 0, nb_il = 0;
+  if (t + 3 * GW < T) brows_bounds<V, EI>(P, q, t + 3 * GW, T, cnt, nb_i0, nb_il);
   // relaxations (solver.py:297, :372) of this thread's lanes: LPT 8/16-bit
   // counters packed in one register (a thread sees STEPS <= 16 edges per tile),
   // flushed into accR after every tile
@@ -568,7 +589,10 @@ __device__ void bphase_expand(const BParams<V, EI>& P, int q, uint32_t r, const 
     if (have_rn) {
       btile_issue<V, EI>(P, t + GW, E, lane, Rn, Bt);
       have_rn = t + 2 * GW < T;
-      if (have_rn) brows_load<V, EI, LIVE>(P, q, t + 2 * GW, T, cnt, lane, Rn);
+      if (have_rn) {
+        brows_finish<V, EI, LIVE>(P, q, nb_i0, nb_il, lane, Rn);
+        if (t + 3 * GW < T) brows_bounds<V, EI>(P, q, t + 3 * GW, T, cnt, nb_i0, nb_il);
+      }
     }
   }
 }
