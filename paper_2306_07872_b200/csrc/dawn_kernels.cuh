@@ -591,6 +591,7 @@ __device__ void phase_expand(const KParams<V, EI>& P, int p, uint32_t r, bool de
   EI pf_base = 0, pf_off = 0;
   K pf_key = 0;
   uint32_t pf_node = 0;
+  bool pf_live = false;  // async: pf_key of the next tile still to load from pf_node
   if (lane <= il - i0) {
     pf_base = ldcg(qbase + i0 + lane);
     pf_off = ldcg(qoff + i0 + lane);
@@ -645,9 +646,13 @@ __device__ void phase_expand(const KParams<V, EI>& P, int p, uint32_t r, bool de
         if (lane <= il - i0) {
           pf_base = ldcg(qbase + i0 + lane);
           pf_off = ldcg(qoff + i0 + lane);
-          pf_key = (!PRED && P.live) ? ldcg(P.dist + ldcg(qnode + i0 + lane)) : ldcg(qkey + i0 + lane);
+          // async: only the node here; its live value is loaded after this tile's
+          // edge loads are issued (the dependent load stalled the warp mid-tile)
+          if (!PRED && P.live) pf_node = ldcg(qnode + i0 + lane);
+          else pf_key = ldcg(qkey + i0 + lane);
           if (PRED) pf_node = ldcg(qnode + i0 + lane);
         }
+        pf_live = !PRED && P.live && lane <= il - i0;
         tr = (lane < 2 && tn + GW < T) ? row_bound(tn + GW, lane) : 0u;
       }
     }
@@ -714,6 +719,10 @@ __device__ void phase_expand(const KParams<V, EI>& P, int p, uint32_t r, bool de
       const EI safe0 = __shfl_sync(0xffffffffu, c_base, 0) + e0;  // the tile's first edge
 #pragma unroll
       for (int j = 0; j < XI; ++j) EdgeAccess<V>::load(P, ((okm >> j) & 1u) ? pos[j] : safe0, col[j], wv[j]);
+    }
+    if (!PRED && pf_live) {  // the next tile's live row values (its nodes arrived meanwhile)
+      pf_key = ldcg(P.dist + pf_node);
+      pf_live = false;
     }
     // ---- phase 2: candidates ----
     K cand[XI];
