@@ -23,6 +23,9 @@ KEYS = [
     ("dram__bytes_read.sum", "DRAM read"),
     ("dram__bytes_write.sum", "DRAM write"),
     ("dram__throughput.avg.pct_of_peak_sustained_elapsed", "DRAM throughput % of peak"),
+    ("FBSP.TriageCompute.dram__throughput.avg.pct_of_peak_sustained_elapsed", "DRAM throughput % of peak"),
+    ("dram__bytes.sum.per_second", "DRAM bandwidth achieved"),
+    ("gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed", "memory throughput % of peak (max unit)"),
     ("lts__t_sectors_srcunit_tex_op_read.sum", "L2 read sectors from L1"),
     ("lts__t_sector_hit_rate.pct", "L2 hit rate"),
     ("lts__throughput.avg.pct_of_peak_sustained_elapsed", "L2 throughput % of peak"),
