@@ -523,35 +523,36 @@ __device__ void bphase_expand(const BParams<V, EI>& P, int q, uint32_t r, const 
       }
     } else {
     // ---- relax tile A ----
-    uint32_t ck = 0xFFFFFFFFu;  // this thread's current row (relative to A.i0)
-    K cs[LPT];
-#pragma unroll
-    for (int i = 0; i < LPT; ++i) cs[i] = 0;
     uint32_t rcp = 0;
 #pragma unroll 1
     for (int q0 = 0; q0 < STEPS; q0 += U) {
       if ((uint32_t)(q0 * EPW) >= A.len) break;  // warp-uniform
       K cand[U][LPT], cur[U][LPT];
       uint32_t vq[U], am[U];
+      WB wq[U];
+      // every load of the U steps first — the rows' own lines (snapshot, or the
+      // live line under async) into cand[], the targets' lines into cur[] —
+      // then the candidates: a row line loaded inside the step and consumed at
+      // once serialised the steps of short-row tiles
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const uint32_t j = (uint32_t)((q0 + u) * EPW) + eg;
         vq[u] = __shfl_sync(0xffffffffu, A.col, j & 31);
         const uint32_t kq = __shfl_sync(0xffffffffu, A.kr, j & 31);
-        const WB wq = shfl_any<WB>(A.w, j & 31);
+        wq[u] = shfl_any<WB>(A.w, j & 31);
         const uint32_t mq = __shfl_sync(0xffffffffu, A.rmask, kq & 31);
         const uint32_t nq = LIVE ? __shfl_sync(0xffffffffu, A.rnode, kq & 31) : 0u;
         const uint32_t a = (j < A.len) ? ((mq >> lsh) & LMASK) : 0u;
-        if (kq != ck) {  // the row's snapshot, or (async) its live line (L1)
-          ck = kq;
-          ld16_ca<K, LPT>((LIVE ? P.bd + (size_t)nq * BL : P.qkey + (size_t)(A.i0 + kq) * BL) + lsh, cs);
-        }
-#pragma unroll
-        for (int i = 0; i < LPT; ++i) cand[u][i] = CD::relax(CD::dec(cs[i]), wq);
+        ld16_ca<K, LPT>((LIVE ? P.bd + (size_t)nq * BL : P.qkey + (size_t)(A.i0 + kq) * BL) + lsh, cand[u]);
         rcp += (a * SPREAD) & FMASK;
         am[u] = a;
         // inactive threads re-read the tile's first line (an L1 hit) instead of branching
         ld16_ca<K, LPT>(P.bd + (size_t)(a ? vq[u] : vq[0]) * BL + lsh, cur[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+#pragma unroll
+        for (int i = 0; i < LPT; ++i) cand[u][i] = CD::relax(CD::dec(cand[u][i]), wq[u]);
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
