@@ -147,16 +147,12 @@ def load_matrix_market(stream: Iterable[str]) -> EdgeList:
 
 
 def _edge_lines(g: CsrGraph, base: int) -> str:
-    """``u v w`` lines in CSR order, ``%.17g`` weights (native formatter)."""
-    from .solver import format_distance_rows
-
+    """``u v w`` lines in CSR order with ``%.17g`` weights (graph.py:339-356)."""
     if g.m == 0:
         return ""
     u = np.repeat(np.arange(g.n, dtype=np.int64), np.diff(np.asarray(g.row_ptr, dtype=np.int64))) + base
     v = np.asarray(g.col, dtype=np.int64) + base
-    # one "row" per edge: source = u, values = [w]; then splice v in between
-    w_txt = format_distance_rows(np.asarray(g.val, dtype=np.float64)[:, None], u.tolist()).splitlines()
-    return "".join(f"{line.split(',', 1)[0]} {b} {line.split(',', 1)[1]}\n" for line, b in zip(w_txt, v.tolist()))
+    return "".join("%d %d %.17g\n" % t for t in zip(u.tolist(), v.tolist(), np.asarray(g.val, dtype=np.float64).tolist()))
 
 
 def write_edge_list(g: CsrGraph, fh: IO[str]) -> None:
