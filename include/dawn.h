@@ -236,6 +236,13 @@ int dawn_gen_rmat(int device, int scale, int64_t edge_factor, double a, double b
                   uint64_t seed, int wkind, int64_t wlo, int64_t whi, uint64_t wseed,
                   int64_t* u_out, int64_t* v_out, double* w_out, void* stream);
 
+/* 4-neighbour grid of rows x cols nodes (id = r*cols + c), both directions,
+ * written directly in canonical CSR order (no sort): row_ptr_out[n+1],
+ * col_out / val_out [m], m = 4*rows*cols - 2*rows - 2*cols.  Bit-identical
+ * to generators.grid_graph (weights drawn per CSR position). */
+int dawn_gen_grid(int device, int64_t rows, int64_t cols, int wkind, int64_t wlo, int64_t whi,
+                  uint64_t wseed, int64_t* row_ptr_out, int64_t* col_out, double* val_out, void* stream);
+
 /* Dense all-pairs Floyd–Warshall on the device: floyd_warshall_apsp
  * (oracles.py:141-162), the cross-check oracle, float64, same step order and
  * rounding as the NumPy loop (not blocked).  Input: the CsrGraph arrays

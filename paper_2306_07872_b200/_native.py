@@ -63,6 +63,7 @@ EXPORTS = (
     "dawn_mssp_batch",
     "dawn_build_csr",
     "dawn_gen_rmat",
+    "dawn_gen_grid",
     "dawn_oracle_dijkstra",
     "dawn_oracle_bellman_ford",
 )
@@ -121,6 +122,8 @@ def _declare(L: ctypes.CDLL) -> None:
                                    c_void_p, c_void_p]),
         "dawn_gen_rmat": (c_int, [c_int, c_int, c_int64, c_double, c_double, c_double, c_uint64, c_int,
                                   c_int64, c_int64, c_uint64, c_void_p, c_void_p, c_void_p, c_void_p]),
+        "dawn_gen_grid": (c_int, [c_int, c_int64, c_int64, c_int, c_int64, c_int64, c_uint64, c_void_p, c_void_p,
+                                  c_void_p, c_void_p]),
         "dawn_oracle_dijkstra": (c_int, [c_int64, c_void_p, c_void_p, c_void_p, c_int64, c_void_p, P64]),
         "dawn_oracle_bellman_ford": (c_int, [c_int64, c_void_p, c_void_p, c_void_p, c_int64, c_void_p, P64,
                                              POINTER(c_int)]),

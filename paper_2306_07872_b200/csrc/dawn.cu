@@ -1642,6 +1642,56 @@ extern "C" int dawn_gen_rmat(int device, int scale, int64_t edge_factor, double 
   return DAWN_OK;
 }
 
+// 4-neighbour grid written straight into CSR (grid_graph, generators.py:96-113).
+// Row offsets are closed-form: a node in grid row i loses one edge per border
+// it touches, so rows before i hold i(4C-2) - C[i>0] edges and the nodes
+// before column j of row i hold j(4 - t_i) - [j>0], t_i = [i==0] + [i==R-1].
+// Neighbours in ascending id (up, left, right, down); the weight of the edge
+// at CSR position e is the same counter draw as the RMAT weights.
+__global__ void k_gen_grid(int64_t R, int64_t C, int wkind, int64_t wlo, unsigned long long wrange,
+                           unsigned long long wseed, int64_t* row_ptr, int64_t* col, double* val) {
+  const int64_t n = R * C;
+  for (int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; id <= n;
+       id += (int64_t)gridDim.x * blockDim.x) {
+    if (id == n) {
+      row_ptr[n] = 4 * R * C - 2 * R - 2 * C;
+      continue;
+    }
+    const int64_t i = id / C, j = id - i * C;
+    const int64_t t = (i == 0) + (i == R - 1);
+    int64_t e = i * (4 * C - 2) - (i > 0 ? C : 0) + j * (4 - t) - (j > 0);
+    row_ptr[id] = e;
+    const int64_t nb[4] = {i > 0 ? id - C : -1, j > 0 ? id - 1 : -1, j + 1 < C ? id + 1 : -1,
+                           i + 1 < R ? id + C : -1};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (nb[k] < 0) continue;
+      const unsigned long long h = draw64(wseed, (unsigned long long)e, 63);
+      col[e] = nb[k];
+      val[e] = wkind == 0 ? (double)(wlo + (int64_t)(((h >> 32) * wrange) >> 32))
+                          : (double)((float)(h >> 40) * (1.0f / 16777216.0f));
+      ++e;
+    }
+  }
+}
+
+extern "C" int dawn_gen_grid(int device, int64_t rows, int64_t cols, int wkind, int64_t wlo, int64_t whi,
+                             uint64_t wseed, int64_t* row_ptr_out, int64_t* col_out, double* val_out,
+                             void* stream) {
+  if (rows < 1 || cols < 1 || rows > (1ll << 31) / cols || !row_ptr_out ||
+      ((rows > 1 || cols > 1) && (!col_out || !val_out)))
+    return fail(DAWN_EINVAL, "bad grid arguments");
+  if (wkind == 0 && (whi < wlo || whi - wlo >= (1ll << 32))) return fail(DAWN_EINVAL, "bad weight range");
+  CK(cudaSetDevice(device));
+  const int64_t n = rows * cols;
+  const int blocks = (int)std::min<int64_t>((n + 256) / 256, 148 * 16);
+  k_gen_grid<<<blocks, 256, 0, (cudaStream_t)stream>>>(rows, cols, wkind, wlo,
+                                                       (unsigned long long)(whi - wlo + 1), wseed,
+                                                       row_ptr_out, col_out, val_out);
+  CK(cudaGetLastError());
+  return DAWN_OK;
+}
+
 // ---------------------------------------------------------------------------
 // Floyd–Warshall on the device (floyd_warshall_apsp, oracles.py:141-162)
 // ---------------------------------------------------------------------------

@@ -95,3 +95,34 @@ def rmat_device_graph(scale: int, edge_factor: int, weights: str = "f32", precis
     deg = (rp[1:] - rp[:-1]).clone()
     del rp, col, val
     return dg, host, deg
+
+
+def grid_csr_device(rows: int, cols: int, weights: str = "int", lo: int = 1, hi: int = 100, wseed: int = 2,
+                    device: int = 0):
+    """``grid_graph`` (generators.py) written straight into CSR on the device
+    by ``dawn_gen_grid``: (n, m, row_ptr, col, val) CUDA tensors."""
+    import torch
+
+    n = rows * cols
+    m = 4 * rows * cols - 2 * rows - 2 * cols
+    dev = torch.device("cuda", device)
+    rp = torch.empty(n + 1, dtype=torch.int64, device=dev)
+    col = torch.empty(max(m, 1), dtype=torch.int64, device=dev)
+    val = torch.empty(max(m, 1), dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    N.check(N.lib().dawn_gen_grid(device, rows, cols, 0 if weights == "int" else 1, lo, hi, wseed, rp.data_ptr(),
+                                  col.data_ptr(), val.data_ptr(), stream))
+    return n, m, rp, col[:m], val[:m]
+
+
+def grid_device_graph(rows: int, cols: int, precision: str = "fp32", device: int = 0, keep_host: bool = False,
+                      **kw):
+    """A resident ``DeviceGraph`` of the grid (no host build, no sort);
+    optionally also the host ``CsrGraph``."""
+    n, m, rp, col, val = grid_csr_device(rows, cols, device=device, **kw)
+    vt = {"fp32": N.F32, "fp64": N.F64, "int32": N.I32}[precision]
+    dg = DeviceGraph.from_device_arrays(n, m, rp, col, val, vt, device)
+    host = None
+    if keep_host:
+        host = CsrGraph(n=n, m=m, row_ptr=rp.cpu().numpy(), col=col.cpu().numpy(), val=val.cpu().numpy())
+    return dg, host

@@ -90,3 +90,32 @@ def test_rmat_device_equals_reference_arm_generator(gpu, scale, ef, weights):
     assert (n, m) == (on, om)
     assert np.array_equal(rp.cpu().numpy(), orp) and np.array_equal(col.cpu().numpy(), ocol)
     assert np.array_equal(val.cpu().numpy(), oval)
+
+
+@pytest.mark.parametrize("rows,cols", [(1, 1), (1, 7), (9, 1), (2, 2), (3, 4), (57, 91), (300, 300), (1024, 1024)])
+def test_grid_device_equals_host_generator(gpu, rows, cols):
+    """dawn_gen_grid (closed-form CSR offsets, no sort) == generators.grid_graph."""
+    host = G.grid_graph(rows, cols)
+    n, m, rp, col, val = D.grid_csr_device(rows, cols)
+    dev = P.CsrGraph(n=n, m=m, row_ptr=rp.cpu().numpy(), col=col.cpu().numpy(), val=val.cpu().numpy())
+    assert same_graph(dev, host)
+
+
+def test_grid_device_float_weights_and_solve(gpu):
+    host = G.grid_graph(40, 50)
+    n, m, rp, col, val = D.grid_csr_device(40, 50, weights="f32")
+    assert np.array_equal(rp.cpu().numpy(), host.row_ptr) and np.array_equal(col.cpu().numpy(), host.col)
+    assert np.array_equal(val.cpu().numpy(), G._weights(m, 2, "f32", 1, 100))
+    dg, h2 = D.grid_device_graph(40, 50, precision="int32", keep_host=True)
+    assert same_graph(h2, host) and (dg.n, dg.m) == (host.n, host.m)
+    dg.close()
+
+
+def test_grid_device_rejects_bad_shape(gpu):
+    import ctypes
+
+    from paper_2306_07872_b200 import _native as N
+
+    assert N.lib().dawn_gen_grid(0, 0, 5, 0, 1, 100, 2, None, None, None, None) != 0
+    assert N.lib().dawn_gen_grid(0, 3, 3, 0, 5, 1, 2, ctypes.c_void_p(8), ctypes.c_void_p(8), ctypes.c_void_p(8),
+                                 None) != 0
