@@ -14,7 +14,7 @@
 //   B (build): a coalesced sweep over nmask[v] = lanes that lowered v in
 //      round r-1.  It clears nmask, does the write bookkeeping of round r-1
 //      (writes, first discoveries, nodes lowered in >= 2 rounds: per-lane
-//      counts via warp REDUX, no atomics), and lays the frontier of round r
+//      counts via bit-sliced adds + warp bit transposes, no atomics), and lays the frontier of round r
 //      out as entries {node, lane mask, edge offset, row base} plus a
 //      32-lane snapshot of the row's distances (the value each lane relaxes
 //      with, as of the start of the round).  GOVM: lane mask = lanes that
@@ -129,6 +129,54 @@ __device__ __forceinline__ T shfl_any(T v, int src) {
   }
 }
 
+#ifndef DAWN_BATCH_CUR_CG
+#define DAWN_BATCH_CUR_CG 1  // target lines through L2 only (ld.cg): fresher values, L1 kept for the row lines
+#endif
+
+#ifndef DAWN_BATCH_BKSLICE
+#define DAWN_BATCH_BKSLICE 1  // per-lane write counts by bit-sliced adds + warp bit transposes
+#endif
+
+__device__ __forceinline__ uint32_t maj3(uint32_t a, uint32_t b, uint32_t c) { return (a & b) | (c & (a ^ b)); }
+
+// per-bit counts (0..8) of eight lane masks as four bit planes (carry-save adder tree)
+__device__ __forceinline__ void csa8(const uint32_t (&q)[ITEMS], uint32_t (&p)[4]) {
+  static_assert(ITEMS == 8, "csa8 sums eight masks");
+  const uint32_t s1 = q[0] ^ q[1] ^ q[2], c1 = maj3(q[0], q[1], q[2]);
+  const uint32_t s2 = q[3] ^ q[4] ^ q[5], c2 = maj3(q[3], q[4], q[5]);
+  const uint32_t s3 = q[6] ^ q[7], c3 = q[6] & q[7];
+  p[0] = s1 ^ s2 ^ s3;
+  const uint32_t c4 = maj3(s1, s2, s3);
+  const uint32_t s5 = c1 ^ c2 ^ c3, c5 = maj3(c1, c2, c3);
+  p[1] = s5 ^ c4;
+  const uint32_t c6 = s5 & c4;
+  p[2] = c5 ^ c6;
+  p[3] = c5 & c6;
+}
+
+// 32x32 bit transpose across the warp: lane b returns the word whose bit t is
+// bit b of lane t's x
+__device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, uint32_t lane) {
+  constexpr uint32_t MK[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
+#pragma unroll
+  for (int s = 0; s < 5; ++s) {
+    const uint32_t j = 16u >> s, m = MK[s];
+    const uint32_t y = __shfl_xor_sync(0xffffffffu, x, j);
+    x = (lane & j) ? ((x & ~m) | ((y & ~m) >> j)) : ((x & m) | ((y & m) << j));
+  }
+  return x;
+}
+
+// lane b: how many of the warp's 32 x 8 masks have bit b set
+__device__ __forceinline__ uint32_t warp_bitcount8(const uint32_t (&q)[ITEMS], uint32_t lane) {
+  uint32_t p[4];
+  csa8(q, p);
+  uint32_t c = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) c += (uint32_t)__popc(warp_transpose32(p[i], lane)) << i;
+  return c;
+}
+
 // ---------------------------------------------------------------------------
 // B phase: consume nmask (round r-1's writes), build round r's frontier
 // ---------------------------------------------------------------------------
@@ -196,6 +244,15 @@ __device__ void bphase_build(const BParams<V, EI>& P, uint32_t r, uint32_t activ
             if (u0 + j < n) { P.w1[u0 + j] = W1[j]; P.w2[u0 + j] = W2[j]; P.nmask[u0 + j] = 0u; }
         }
       }
+#if DAWN_BATCH_BKSLICE
+      // per-lane counts: lane b sums bit b over the warp's 256 nodes — the eight
+      // masks of a thread added bit-sliced, the planes transposed across the warp
+      if (__any_sync(0xffffffffu, anyM != 0u)) {
+        accW += warp_bitcount8(M, lane);
+        accFD += warp_bitcount8(FDm, lane);
+        accMW += warp_bitcount8(MWm, lane);
+      }
+#else
       // per-lane counts: lane b sums bit b over the warp's nodes (one REDUX per bit)
 #pragma unroll 1
       for (int j = 0; j < ITEMS; ++j) {
@@ -212,6 +269,7 @@ __device__ void bphase_build(const BParams<V, EI>& P, uint32_t r, uint32_t activ
           }
         }
       }
+#endif
     } else if (anyM) {
       if (full) {
         reinterpret_cast<uint4*>(P.nmask + u0)[0] = make_uint4(0, 0, 0, 0);
@@ -349,8 +407,8 @@ struct BLanes {
 };
 
 template <class K, int LPT>
-__device__ __forceinline__ void ld16_ca(const K* p, K (&o)[LPT]) {
-  const uint4 x = __ldca(reinterpret_cast<const uint4*>(p));
+__device__ __forceinline__ void ld16_ca(const K* p, K (&o)[LPT], bool cg = false) {
+  const uint4 x = cg ? __ldcg(reinterpret_cast<const uint4*>(p)) : __ldca(reinterpret_cast<const uint4*>(p));
   if constexpr (LPT == 4) {
     o[0] = (K)x.x; o[1] = (K)x.y; o[2] = (K)x.z; o[3] = (K)x.w;
   } else {
@@ -547,7 +605,7 @@ __device__ void bphase_expand(const BParams<V, EI>& P, int q, uint32_t r, const 
         rcp += (a * SPREAD) & FMASK;
         am[u] = a;
         // inactive threads re-read the tile's first line (an L1 hit) instead of branching
-        ld16_ca<K, LPT>(P.bd + (size_t)(a ? vq[u] : vq[0]) * BL + lsh, cur[u]);
+        ld16_ca<K, LPT>(P.bd + (size_t)(a ? vq[u] : vq[0]) * BL + lsh, cur[u], DAWN_BATCH_CUR_CG != 0);
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
