@@ -604,8 +604,10 @@ __device__ void bphase_expand(const BParams<V, EI>& P, int q, uint32_t r, const 
         ld16_ca<K, LPT>((LIVE ? P.bd + (size_t)nq * BL : P.qkey + (size_t)(A.i0 + kq) * BL) + lsh, cand[u]);
         rcp += (a * SPREAD) & FMASK;
         am[u] = a;
-        // inactive threads re-read the tile's first line (an L1 hit) instead of branching
-        ld16_ca<K, LPT>(P.bd + (size_t)(a ? vq[u] : vq[0]) * BL + lsh, cur[u], DAWN_BATCH_CUR_CG != 0);
+        // threads without an active lane still read their part of the edge's own
+        // target line (unpredicated, one request per line; predicating them off or
+        // pointing them at another line was slower)
+        ld16_ca<K, LPT>(P.bd + (size_t)vq[u] * BL + lsh, cur[u], DAWN_BATCH_CUR_CG != 0);
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
