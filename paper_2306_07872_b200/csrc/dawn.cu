@@ -181,6 +181,10 @@ struct dawn_solver_s {
   int grid_pred = 1;  // ... of the predecessor-tracking instance
   size_t smem = 0;
   double dense_edges_per_node = 0.5;  // tunable: dense frontier build after rounds relaxing >= this * n edges
+  uint32_t* phist = nullptr;          // priority window histograms [2][PW_BINS]
+  double pw_frac = 0.35;              // tunable "priority_frac": heavy async rounds relax the lowest this share
+                                      // of the frontier's edges by row value (0 = off)
+  double pw_edges_per_edge = 0.25;    // tunable "priority_edges_per_edge": ... rounds relaxing >= this * m edges
   int wide_pref = -1;                 // tunable "wide_tiles": -1 auto, 0 narrow, 1 wide X-phase tiles
   bool wide = false;
   int fb_pref = -1;                   // tunable "bitmap_frontier": -1 auto, 0 off, 1 on
@@ -636,6 +640,11 @@ struct Impl {
     if (!(P.nf_delta > 0)) P.nf_delta = std::is_floating_point<V>::value ? 1e-3 : 1.0;
     P.nf_cap = (uint32_t)std::min(s->nf_cap, 4.0e9);
     P.skip_if_done = 0;
+    P.phist = s->phist;
+    P.pw_frac = (float)s->pw_frac;
+    P.pw_edges = std::max(P.dense_edges, (unsigned long long)std::max(1.0, s->pw_edges_per_edge * (double)g->m));
+    P.pw = (P.live && P.algo == 0 && !g->has_negative && sizeof(K) == 4 && !P.pred_on && !s->fb &&
+            max_rounds == 0xFFFFFFFFu && s->phist != nullptr && s->pw_frac > 0.0 && s->pw_frac < 1.0) ? 1 : 0;
     return P;
   }
 
@@ -1014,6 +1023,8 @@ struct Impl {
     const size_t ks = sizeof(K), es = sizeof(EI);
     CK(dmalloc(&s->dist, ks * n));
     CK(dmalloc(&s->stamp, 4 * n));
+    CK(dmalloc(&s->phist, 4 * 2 * PW_BINS));
+    CK(cudaMemset(s->phist, 0, 4 * 2 * PW_BINS));
     CK(dmalloc(&s->bmap, 4 * (size_t)((n + 31) / 32 + 4)));  // padded for 16-byte loads
     CK(dmalloc(&s->wstate, (size_t)n + 4));  // + 4: the worklist tail updates it by 32-bit words
     if (!s->g->has_negative) {
@@ -1073,6 +1084,7 @@ static void solver_free(dawn_solver_t s) {
   cudaDeviceSynchronize();
   dfree(s->dist);
   dfree(s->stamp);
+  dfree(s->phist);
   dfree(s->bmap);
   dfree(s->wstate);
   dfree(s->pred);
@@ -1184,6 +1196,16 @@ extern "C" int dawn_solver_tune(dawn_solver_t s, const char* key, double value) 
   if (!strcmp(key, "nearfar_batches")) {
     if (!(value >= 0.0)) return fail(DAWN_EINVAL, "nearfar_batches must be >= 0");
     s->nf_cap = value;
+    return DAWN_OK;
+  }
+  if (!strcmp(key, "priority_frac")) {
+    if (!(value >= 0.0 && value <= 1.0)) return fail(DAWN_EINVAL, "priority_frac must be in [0, 1]");
+    s->pw_frac = value;
+    return DAWN_OK;
+  }
+  if (!strcmp(key, "priority_edges_per_edge")) {
+    if (!(value >= 0.0)) return fail(DAWN_EINVAL, "priority_edges_per_edge must be >= 0");
+    s->pw_edges_per_edge = value;
     return DAWN_OK;
   }
   if (!strcmp(key, "nearfar_delta_mean")) {

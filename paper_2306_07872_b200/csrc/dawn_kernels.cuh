@@ -74,6 +74,14 @@ struct KParams {
   unsigned long long* wl_ring;         // ring of 16-byte row items (uint4); nullptr = off
   unsigned long long wl_mask;          // ring capacity - 1 (power of two)
   unsigned long long wl_edges;
+  // priority window (async GOVM, non-negative 4-byte values, unbounded run): a
+  // heavy round relaxes only the frontier rows whose live value lies in the
+  // lowest pw_frac of the frontier's edges (degree-weighted histogram built by
+  // the dense S phase); the others are deferred to the next round
+  int pw;                              // on for this run
+  float pw_frac;
+  unsigned long long pw_edges;         // rounds relaxing >= this many edges apply the window
+  uint32_t* phist;                     // [2][PW_BINS] degree-weighted value histograms, by round parity
   double nf_delta;                     // near-far schedule: bucket width in weight units (dawn_nearfar.cuh)
   uint32_t nf_cap;                     // near-far: continuation batches a warp may run per round
 };
@@ -107,7 +115,27 @@ struct __align__(16) Smem {
   unsigned long long scr64[WPB];
   unsigned long long basepk;
   uint32_t claim[2];  // dense S phase: the chunk after next (double-buffered by iteration)
+  uint32_t pw_tb;     // priority window: last histogram bin relaxed this round
 };
+
+// Priority window helpers.  A value's bin is the top 11 bits of its float32
+// representation (exponent + 2 mantissa bits: bins ~19 % wide), monotone for
+// the non-negative values the window runs on.  A deferred frontier row keeps
+// stamp (r | STAMP_DEFER): the next dense S phase selects it again without
+// counting it as a write of round r.
+constexpr int PW_BINS = 1024;
+constexpr uint32_t STAMP_DEFER = 0x80000000u;
+template <class C>
+__device__ __forceinline__ uint32_t pw_bin(C v) {
+  const uint32_t b = __float_as_uint((float)v) >> 21;
+  return b < (uint32_t)PW_BINS ? b : (uint32_t)(PW_BINS - 1);
+}
+template <class V, class K>
+__device__ __forceinline__ uint32_t pw_bin_key(K key) {  // raw (non-negative) keys only
+  if constexpr (std::is_same<V, float>::value) return pw_bin(__uint_as_float((uint32_t)key));
+  else if constexpr (std::is_same<V, double>::value) return pw_bin(__longlong_as_double((long long)key));
+  else return pw_bin((V)key);
+}
 
 template <class V> struct EdgeAccess;
 template <> struct EdgeAccess<int32_t> {  // 4-byte value types: one 8-byte load per edge
@@ -242,7 +270,7 @@ __device__ __forceinline__ void ldg8(const T* p, T (&o)[ITEMS]) {
 template <class V, class EI, int XI>
 __device__ void phase_compact(const KParams<V, EI>& P, int p, uint32_t r, Smem<V, EI, XI>& s,
                               unsigned long long& acc_w, unsigned long long& acc_fd,
-                              unsigned long long& acc_multi, uint32_t& prev_w) {
+                              unsigned long long& acc_multi, uint32_t& prev_w, uint32_t tb = 0xFFFFFFFFu) {
   using VT = Val<V>;
   using K = typename VT::K;
   const uint32_t n = P.n;
@@ -250,7 +278,7 @@ __device__ void phase_compact(const KParams<V, EI>& P, int p, uint32_t r, Smem<V
   const bool gsvm = P.algo == 1;
   const int eb = P.ebits;
   // keys: the snapshot values (Jacobi) and GSVM's finite test; the async schedule's GOVM needs neither
-  const bool need_keys = gsvm || !P.live;
+  const bool need_keys = gsvm || !P.live || tb != 0xFFFFFFFFu;
   // Everything a chunk needs — stamps, write states, keys, row bounds — is
   // loaded one iteration ahead, unconditionally: a CTA walks ~7 chunks per
   // phase and a per-chunk chain of dependent loads (stamps -> keys/rows/state)
@@ -303,21 +331,34 @@ __device__ void phase_compact(const KParams<V, EI>& P, int p, uint32_t r, Smem<V
     const K (&keys)[ITEMS] = cur.keys;
     const EI (&rp)[ITEMS + 1] = cur.rp;
     const bool full = u0 + ITEMS <= n;
-    unsigned wm = 0;  // lowered in round r-1
+    unsigned wm = 0, dm = 0;  // lowered in round r-1 / deferred by it (priority window)
 #pragma unroll
     for (int j = 0; j < ITEMS; ++j) wm |= (unsigned)(cur.st[j] == r - 1 && u0 + j < n) << j;
-    const unsigned want = gsvm ? ((u0 < n) ? 0xFFu : 0u) : wm;
-    unsigned sel = 0;
+    if (P.pw) {
+#pragma unroll
+      for (int j = 0; j < ITEMS; ++j) dm |= (unsigned)(cur.st[j] == ((r - 1) | STAMP_DEFER) && u0 + j < n) << j;
+    }
+    const unsigned want = gsvm ? ((u0 < n) ? 0xFFu : 0u) : (wm | dm);
+    unsigned sel = 0, dfr = 0;
     uint32_t mycnt = 0;
     EI mydeg = 0;
     if (want) {
 #pragma unroll
       for (int j = 0; j < ITEMS; ++j) {
         if (((want >> j) & 1u) && u0 + j < n && keys[j] != VT::INF && rp[j + 1] > rp[j]) {
-          sel |= 1u << j;
-          mycnt++;
-          mydeg += rp[j + 1] - rp[j];
+          if (tb != 0xFFFFFFFFu && pw_bin_key<V>(keys[j]) > tb) {
+            dfr |= 1u << j;  // priority window: relaxed in a later round
+          } else {
+            sel |= 1u << j;
+            mycnt++;
+            mydeg += rp[j + 1] - rp[j];
+          }
         }
+      }
+      if (dfr) {
+#pragma unroll
+        for (int j = 0; j < ITEMS; ++j)
+          if ((dfr >> j) & 1u) P.stamp[u0 + j] = r | STAMP_DEFER;
       }
     }
     // write bookkeeping for round r-1 (first_discoveries, >= 2-round nodes)
@@ -370,6 +411,75 @@ __device__ void phase_compact(const KParams<V, EI>& P, int p, uint32_t r, Smem<V
     c = cn;
     cn = s.claim[it & 1];  // written before this iteration's barriers
   }
+}
+
+// Priority window, first pass of a heavy round's S phase: the degree-weighted
+// histogram of the frontier's values (rows lowered or deferred in round r-1).
+template <class V, class EI, int XI>
+__device__ void phase_hist(const KParams<V, EI>& P, int p, uint32_t r, Smem<V, EI, XI>& s) {
+  using K = typename Val<V>::K;
+  uint32_t* hist = reinterpret_cast<uint32_t*>(&s.w[0]);  // the S phase does not use the warp marks
+  static_assert(sizeof(s.w) >= PW_BINS * sizeof(uint32_t), "histogram overlays the warp marks");
+  for (int i = threadIdx.x; i < PW_BINS; i += NT) hist[i] = 0u;
+  __syncthreads();
+  const uint32_t n = P.n;
+  const uint32_t nchunks = (n + TILE - 1) / TILE;
+  for (uint32_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+    const uint32_t u0 = c * TILE + threadIdx.x * ITEMS;
+    if (u0 >= n) continue;
+    uint32_t st[ITEMS];
+    K keys[ITEMS];
+    EI rp[ITEMS + 1];
+    if (u0 + ITEMS <= n) {
+      ldcg8<uint32_t>(P.stamp + u0, st);
+      ldcg8<K>(P.dist + u0, keys);
+      ldg8<EI>(P.row_ptr + u0, *reinterpret_cast<EI(*)[ITEMS]>(rp));
+      rp[ITEMS] = __ldg(P.row_ptr + u0 + ITEMS);
+    } else {
+#pragma unroll
+      for (int j = 0; j < ITEMS; ++j) {
+        st[j] = (u0 + j < n) ? ldcg(P.stamp + u0 + j) : 0u;
+        keys[j] = (u0 + j < n) ? ldcg(P.dist + u0 + j) : (K)0;
+        rp[j] = (u0 + j <= n) ? __ldg(P.row_ptr + u0 + j) : (EI)0;
+      }
+      rp[ITEMS] = (u0 + ITEMS <= n) ? __ldg(P.row_ptr + u0 + ITEMS) : (EI)0;
+    }
+#pragma unroll
+    for (int j = 0; j < ITEMS; ++j)
+      if ((st[j] & ~STAMP_DEFER) == r - 1 && u0 + j < n && rp[j + 1] > rp[j])
+        atomicAdd(hist + pw_bin_key<V>(keys[j]), (uint32_t)(rp[j + 1] - rp[j]));
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < PW_BINS; i += NT)
+    if (hist[i]) atomicAdd(P.phist + (size_t)p * PW_BINS + i, hist[i]);
+}
+
+// Priority window: the last bin of round r's histogram inside the lowest
+// pw_frac of its (degree-weighted) mass.  Every thread of the CTA calls it.
+template <class V, class EI, int XI>
+__device__ uint32_t pw_threshold(const KParams<V, EI>& P, int p, Smem<V, EI, XI>& s) {
+  constexpr int BPT = PW_BINS / NT;
+  static_assert(PW_BINS % NT == 0, "bins per thread");
+  const uint32_t* h = P.phist + (size_t)p * PW_BINS + threadIdx.x * BPT;
+  uint32_t b[BPT];
+  unsigned long long mine = 0;
+#pragma unroll
+  for (int i = 0; i < BPT; ++i) { b[i] = ldcg(h + i); mine += b[i]; }
+  unsigned long long tot;
+  const unsigned long long incl = block_incl_sum<unsigned long long>(mine, s.scr64, &tot);
+  const unsigned long long want = (unsigned long long)((double)P.pw_frac * (double)tot);
+  unsigned long long run = incl - mine;
+  if (threadIdx.x == 0) s.pw_tb = PW_BINS - 1;
+  __syncthreads();
+  if (run < want && incl >= want) {  // exactly one thread holds the crossing
+#pragma unroll
+    for (int i = 0; i < BPT; ++i) {
+      run += b[i];
+      if (run >= want) { s.pw_tb = threadIdx.x * BPT + i; break; }
+    }
+  }
+  __syncthreads();
+  return s.pw_tb;
 }
 
 // ---------------------------------------------------------------------------
@@ -1380,10 +1490,13 @@ __global__ void __launch_bounds__(NT, DAWN_MIN_BLOCKS) dawn_persistent(KParams<V
   bool dense_prev = ldcg(&st->dense_prev) != 0u;  // how round r-1 recorded its writes
   bool skip_s = ldcg(&st->resume_x) != 0u;         // stepping: round r's frontier is already built
   unsigned long long acc_w = 0, acc_fd = 0, acc_multi = 0, acc_r = 0;
+  unsigned long long E_prev = 0;  // frontier edges of the previous round (priority window)
+  uint32_t tb = 0xFFFFFFFFu;       // priority window of this round's S phase (0xFFFFFFFF = none)
   unsigned rounds = 0;
   for (;;) {
     const int p = r & 1;
     const bool prof = leader && P.prof != nullptr && r < P.prof_cap;
+    tb = 0xFFFFFFFFu;
     if (!skip_s) {
       if (prof) P.prof[4 * r + 0] = globaltimer();
       // ---- S phase: build round r's frontier ----
@@ -1392,9 +1505,20 @@ __global__ void __launch_bounds__(NT, DAWN_MIN_BLOCKS) dawn_persistent(KParams<V
         st->wround[p] = 0ull;   // writes of round r (counted in X_r or S_{r+1})
         st->sctr[p ^ 1] = 0u;   // chunk counter of S_{r+1} (S_{r-1} used it and is over)
       }
+      if (P.pw && blockIdx.x == 0)  // histogram of round r+1 (X_{r-1} read it before the last barrier)
+        for (int i = threadIdx.x; i < PW_BINS; i += NT) P.phist[(size_t)(p ^ 1) * PW_BINS + i] = 0u;
       if (r >= 2 && (dense_prev || P.algo == 1)) {
         uint32_t prev_w = 0;
-        phase_compact<V, EI, XI>(P, p, r, s, acc_w, acc_fd, acc_multi, prev_w);
+        if constexpr (RAW && !WITH_PRED && !FB) {
+          // priority window: a heavy round's frontier is histogrammed first (one
+          // sweep + barrier), then only its lowest pw_frac (by edges) is selected
+          if (P.pw && r >= 3 && E_prev >= P.pw_edges) {
+            phase_hist<V, EI, XI>(P, p, r, s);
+            if (grid_sync(&st->bar, &st->abort)) break;
+            tb = pw_threshold<V, EI, XI>(P, p, s);
+          }
+        }
+        phase_compact<V, EI, XI>(P, p, r, s, acc_w, acc_fd, acc_multi, prev_w, tb);
         prev_w = __reduce_add_sync(0xffffffffu, prev_w);
         if ((threadIdx.x & 31) == 0 && prev_w) atomicAdd(&st->wround[p ^ 1], (unsigned long long)prev_w);
       } else if (FB && r >= 2) {
@@ -1414,7 +1538,8 @@ __global__ void __launch_bounds__(NT, DAWN_MIN_BLOCKS) dawn_persistent(KParams<V
       if (r >= 2) {
         const unsigned long long wprev = ldcg(&st->wround[p ^ 1]);
         bool stop = false, capflag = false;
-        if (r - 1 >= 2 && wprev == 0) stop = true;                   // a loop round wrote nothing
+        // a loop round wrote nothing (and, under the priority window, deferred nothing)
+        if (r - 1 >= 2 && wprev == 0 && (!P.pw || pk_count(ldcg(&st->res[p]), P.ebits) == 0)) stop = true;
         else if (r - 1 >= P.n) { stop = true; capflag = wprev > 0; }  // cap reached still writing
         if (stop) {
           if (leader) {
@@ -1449,14 +1574,18 @@ __global__ void __launch_bounds__(NT, DAWN_MIN_BLOCKS) dawn_persistent(KParams<V
     skip_s = false;
     // ---- X phase ----
     const unsigned long long E = pk_edges(ldcg(&st->res[p]), P.ebits);
-    const bool dense = P.algo == 1 || E >= P.dense_edges;
+    // a round whose S phase deferred rows records its writes densely (the next
+    // dense S phase picks the deferred rows up again) and never hands over to
+    // the worklist (its queue would miss them)
+    const bool pw_round = tb != 0xFFFFFFFFu;
+    const bool dense = P.algo == 1 || E >= P.dense_edges || pw_round;
     if (prof) {
       P.prof[4 * r + 1] = globaltimer();
       P.prof[4 * r + 3] = ldcg(&st->res[p]);
     }
     if constexpr (RAW && !WITH_PRED && !FB) {
       if (P.wl_ring != nullptr && P.live && P.algo == 0 && P.max_rounds == 0xFFFFFFFFu && r >= 2 &&
-          E < P.wl_edges) {
+          E < P.wl_edges && !pw_round) {
         wl_seed<V, EI>(P, p);
         if (prof) P.prof[4 * r + 2] = globaltimer();  // the seeding; dawn_worklist runs after
         if (leader) {
@@ -1469,6 +1598,7 @@ __global__ void __launch_bounds__(NT, DAWN_MIN_BLOCKS) dawn_persistent(KParams<V
       }
     }
     if (leader) acc_r += E;  // relaxations (solver.py:297, :372)
+    E_prev = E;
     uint32_t round_w = 0;
     phase_expand<V, EI, false, RAW, XI, FB>(P, p, r, dense, s, acc_w, acc_fd, acc_multi, round_w);
     round_w = __reduce_add_sync(0xffffffffu, round_w);
