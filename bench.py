@@ -758,7 +758,9 @@ def ours(args):
                      "own_work_note": "the same formula with this schedule's own R, W"},
         "schedule": {"headline": args.schedule,
                      "note": "async: frontier rows relaxed with their live distance (as the reference's in-place "
-                             "order); identical distances, fewer relaxations, counters timing-dependent. jacobi: "
+                             "order), heavy rounds relax only the rows holding the lowest 35% of the frontier's "
+                             "edges by value (priority window, the rest deferred one round); identical distances, "
+                             "fewer relaxations, counters timing-dependent. jacobi: "
                              "round-start snapshots, counters deterministic and equal to the oracle",
                      "other": other},
         "default_policy_fp64": fp64,
