@@ -182,9 +182,10 @@ struct dawn_solver_s {
   size_t smem = 0;
   double dense_edges_per_node = 0.5;  // tunable: dense frontier build after rounds relaxing >= this * n edges
   uint32_t* phist = nullptr;          // priority window histograms [2][PW_BINS]
-  double pw_frac = 0.35;              // tunable "priority_frac": heavy async rounds relax the lowest this share
+  double pw_frac = 0.2;               // tunable "priority_frac": heavy async rounds relax the lowest this share
                                       // of the frontier's edges by row value (0 = off)
   double pw_edges_per_edge = 0.25;    // tunable "priority_edges_per_edge": ... rounds relaxing >= this * m edges
+  double pw_seed_edges = 4096;        // tunable "priority_seed_edges": a source row this long windows round 2 too
   int wide_pref = -1;                 // tunable "wide_tiles": -1 auto, 0 narrow, 1 wide X-phase tiles
   bool wide = false;
   int fb_pref = -1;                   // tunable "bitmap_frontier": -1 auto, 0 off, 1 on
@@ -643,6 +644,7 @@ struct Impl {
     P.phist = s->phist;
     P.pw_frac = (float)s->pw_frac;
     P.pw_edges = std::max(P.dense_edges, (unsigned long long)std::max(1.0, s->pw_edges_per_edge * (double)g->m));
+    P.pw_seed_edges = (unsigned long long)std::min(std::max(1.0, s->pw_seed_edges), 1.8e19);
     P.pw = (P.live && P.algo == 0 && !g->has_negative && sizeof(K) == 4 && !P.pred_on && !s->fb &&
             max_rounds == 0xFFFFFFFFu && s->phist != nullptr && s->pw_frac > 0.0 && s->pw_frac < 1.0) ? 1 : 0;
     return P;
@@ -1206,6 +1208,11 @@ extern "C" int dawn_solver_tune(dawn_solver_t s, const char* key, double value) 
   if (!strcmp(key, "priority_edges_per_edge")) {
     if (!(value >= 0.0)) return fail(DAWN_EINVAL, "priority_edges_per_edge must be >= 0");
     s->pw_edges_per_edge = value;
+    return DAWN_OK;
+  }
+  if (!strcmp(key, "priority_seed_edges")) {
+    if (!(value >= 0.0)) return fail(DAWN_EINVAL, "priority_seed_edges must be >= 0");
+    s->pw_seed_edges = value;
     return DAWN_OK;
   }
   if (!strcmp(key, "nearfar_delta_mean")) {

@@ -81,6 +81,8 @@ struct KParams {
   int pw;                              // on for this run
   float pw_frac;
   unsigned long long pw_edges;         // rounds relaxing >= this many edges apply the window
+  unsigned long long pw_seed_edges;    // a seeding round relaxing >= this many edges records its writes
+                                       // densely, so round 2 is histogrammed and windowed too
   uint32_t* phist;                     // [2][PW_BINS] degree-weighted value histograms, by round parity
   double nf_delta;                     // near-far schedule: bucket width in weight units (dawn_nearfar.cuh)
   uint32_t nf_cap;                     // near-far: continuation batches a warp may run per round
@@ -469,9 +471,9 @@ __device__ uint32_t pw_threshold(const KParams<V, EI>& P, int p, Smem<V, EI, XI>
   const unsigned long long incl = block_incl_sum<unsigned long long>(mine, s.scr64, &tot);
   const unsigned long long want = (unsigned long long)((double)P.pw_frac * (double)tot);
   unsigned long long run = incl - mine;
-  if (threadIdx.x == 0) s.pw_tb = PW_BINS - 1;
+  if (threadIdx.x == 0) s.pw_tb = tot >= P.pw_edges ? PW_BINS - 1 : 0xFFFFFFFFu;  // light frontier: no window
   __syncthreads();
-  if (run < want && incl >= want) {  // exactly one thread holds the crossing
+  if (tot >= P.pw_edges && run < want && incl >= want) {  // exactly one thread holds the crossing
 #pragma unroll
     for (int i = 0; i < BPT; ++i) {
       run += b[i];
@@ -1492,6 +1494,7 @@ __global__ void __launch_bounds__(NT, DAWN_MIN_BLOCKS) dawn_persistent(KParams<V
   unsigned long long acc_w = 0, acc_fd = 0, acc_multi = 0, acc_r = 0;
   unsigned long long E_prev = 0;  // frontier edges of the previous round (priority window)
   uint32_t tb = 0xFFFFFFFFu;       // priority window of this round's S phase (0xFFFFFFFF = none)
+  bool pw_prev = false;            // the previous round was windowed
   unsigned rounds = 0;
   for (;;) {
     const int p = r & 1;
@@ -1512,7 +1515,9 @@ __global__ void __launch_bounds__(NT, DAWN_MIN_BLOCKS) dawn_persistent(KParams<V
         if constexpr (RAW && !WITH_PRED && !FB) {
           // priority window: a heavy round's frontier is histogrammed first (one
           // sweep + barrier), then only its lowest pw_frac (by edges) is selected
-          if (P.pw && r >= 3 && E_prev >= P.pw_edges) {
+          // (histogrammed after a heavy or windowed round and in round 2 after a
+          // dense seeding round; windowed when the frontier holds >= pw_edges edges)
+          if (P.pw && (r == 2 || E_prev >= P.pw_edges || pw_prev)) {
             phase_hist<V, EI, XI>(P, p, r, s);
             if (grid_sync(&st->bar, &st->abort)) break;
             tb = pw_threshold<V, EI, XI>(P, p, s);
@@ -1578,7 +1583,7 @@ __global__ void __launch_bounds__(NT, DAWN_MIN_BLOCKS) dawn_persistent(KParams<V
     // dense S phase picks the deferred rows up again) and never hands over to
     // the worklist (its queue would miss them)
     const bool pw_round = tb != 0xFFFFFFFFu;
-    const bool dense = P.algo == 1 || E >= P.dense_edges || pw_round;
+    const bool dense = P.algo == 1 || E >= P.dense_edges || pw_round || (P.pw && r == 1 && E >= P.pw_seed_edges);
     if (prof) {
       P.prof[4 * r + 1] = globaltimer();
       P.prof[4 * r + 3] = ldcg(&st->res[p]);
@@ -1599,6 +1604,7 @@ __global__ void __launch_bounds__(NT, DAWN_MIN_BLOCKS) dawn_persistent(KParams<V
     }
     if (leader) acc_r += E;  // relaxations (solver.py:297, :372)
     E_prev = E;
+    pw_prev = pw_round;
     uint32_t round_w = 0;
     phase_expand<V, EI, false, RAW, XI, FB>(P, p, r, dense, s, acc_w, acc_fd, acc_multi, round_w);
     round_w = __reduce_add_sync(0xffffffffu, round_w);

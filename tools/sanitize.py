@@ -73,6 +73,16 @@ def main():
     P.govm_sssp(graphs[0], 0, schedule="async")
     P.set_tuning(nearfar=-1, small_graph=-1)
     checked += 2
+    # the priority window (async, persistent kernel): every round after the first dense one
+    # histogrammed and windowed, on every graph and value type it applies to
+    P.set_tuning(small_graph=0, dense_edges_per_node=0.0, priority_edges_per_edge=0.0)
+    for frac in (0.35, 0.05):
+        P.set_tuning(priority_frac=frac)
+        for g in graphs:
+            for prec in ("auto", "fp32"):
+                P.govm_sssp(g, 0, precision=prec, schedule="async")
+                checked += 1
+    P.set_tuning(small_graph=-1, dense_edges_per_node=0.5, priority_edges_per_edge=0.25, priority_frac=0.2)
     u = rng.integers(0, 1000, 20000)
     v = rng.integers(0, 1000, 20000)
     D.build_csr_device(1000, u, v, rng.uniform(0, 1, 20000))
@@ -80,7 +90,7 @@ def main():
     P.floyd_warshall_apsp(neg if neg.n <= 2000 else graphs[1])
     big = G.rmat_graph(16, 80, weights="f32")  # m >= 2^22: chunked DMA upload path
     P.govm_sssp(big, 0, precision="fp32", schedule="async")
-    print(f"sanitize: {checked} solves (persistent, worklist, near-far, small-graph cluster, speculative negative-weight) + batches + csr build + floyd-warshall + staged upload ran")
+    print(f"sanitize: {checked} solves (persistent, priority window, worklist, near-far, small-graph cluster, speculative negative-weight) + batches + csr build + floyd-warshall + staged upload ran")
 
 
 if __name__ == "__main__":
