@@ -184,7 +184,7 @@ struct dawn_solver_s {
   uint32_t* phist = nullptr;          // priority window histograms [2][PW_BINS]
   double pw_frac = 0.2;               // tunable "priority_frac": heavy async rounds relax the lowest this share
                                       // of the frontier's edges by row value (0 = off)
-  double pw_edges_per_edge = 0.25;    // tunable "priority_edges_per_edge": ... rounds relaxing >= this * m edges
+  double pw_edges_per_edge = 0.4;     // tunable "priority_edges_per_edge": ... rounds relaxing >= this * m edges
   double pw_seed_edges = 4096;        // tunable "priority_seed_edges": a source row this long windows round 2 too
   int wide_pref = -1;                 // tunable "wide_tiles": -1 auto, 0 narrow, 1 wide X-phase tiles
   bool wide = false;

@@ -112,4 +112,4 @@ def test_priority_window_vs_oracle(gpu, frac, weights):
                 assert st.writes >= st.first_discoveries
                 assert not st.negative_cycle
     finally:
-        P.set_tuning(priority_frac=0.2, priority_edges_per_edge=0.25, priority_seed_edges=4096)
+        P.set_tuning(priority_frac=0.2, priority_edges_per_edge=0.4, priority_seed_edges=4096)

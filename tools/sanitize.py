@@ -82,7 +82,7 @@ def main():
             for prec in ("auto", "fp32"):
                 P.govm_sssp(g, 0, precision=prec, schedule="async")
                 checked += 1
-    P.set_tuning(small_graph=-1, dense_edges_per_node=0.5, priority_edges_per_edge=0.25, priority_frac=0.2)
+    P.set_tuning(small_graph=-1, dense_edges_per_node=0.5, priority_edges_per_edge=0.4, priority_frac=0.2)
     u = rng.integers(0, 1000, 20000)
     v = rng.integers(0, 1000, 20000)
     D.build_csr_device(1000, u, v, rng.uniform(0, 1, 20000))
